@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""Fourier LLF throughput on B200 -- the driver's bench contract.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fllf|reference]
+                    [--workload config2|config5]
+
+One step = one pass of the whole hot path (build the 2K+1 pyramids, product-sum,
+collapse) over one batch of synthetic input already resident in HBM.  Default
+workload: BASELINE.json configs[1] (1080x1920 grayscale, 6 levels, K=8,
+T=510, sigma_r=30, m=3), one frame per rank per step; with N ranks each rank
+filters its own frame (frame data-parallel, no collective: "scaling": "weak").
+L2 (126 MB) is flushed between timed steps (a 2x-L2 buffer write, outside the
+per-step events); step durations are CUDA events on the launch stream, summed
+over the K steps, max over ranks.  Rank 0 prints ONE JSON line.
+See DESIGN.md "Measurement" for every key.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Fourier LLF megapixels/sec at K orders, 1/2/4/8 B200; % of HBM roofline"
+UNIT = "MP/s"
+
+WORKLOADS = {
+    "config2": dict(cfg=2, frames=1, desc="BASELINE configs[1]: 1080x1920 gray fp32, 6 levels, K=8, "
+                                          "T=510, sigma_r=30, m=3; 1 frame per rank per step"),
+    "config5": dict(cfg=5, frames=64, desc="BASELINE configs[4]: 64 frames 1080x1920 gray, 6 levels, K=16, "
+                                           "T=510, sigma_r=30, m=3; 64/N frames per rank per step"),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ------------------------------------------------------------------ clocks
+NVML_REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+                0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+                0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+                0x100: "display_clock_setting"}
+
+
+class ClockSampler:
+    """NVML poller (2 ms) for SM clock and clock-event reasons during a region."""
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.ok = [], 0, False
+        self._stop = threading.Event()
+        self._run = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover - no NVML
+            log(f"[bench] NVML unavailable: {e}")
+            self.max_mhz = None
+        self.t = threading.Thread(target=self._loop, daemon=True)
+        self.t.start()
+
+    def _loop(self):
+        while not self._stop.is_set():
+            if self._run.is_set() and self.ok:
+                try:
+                    self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                    self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+                except Exception:
+                    pass
+            time.sleep(0.002)
+
+    def start(self):
+        self._run.set()
+
+    def stop(self):
+        self._run.clear()
+
+    def close(self):
+        self._stop.set()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        names = [n for b, n in NVML_REASONS.items() if self.reasons & b and b != 0x1]
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": names, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- roofline
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def level_dims(H, W, levels):
+    dims = [(H, W)]
+    for _ in range(levels - 1):
+        h, w = dims[-1]
+        dims.append(((h + 1) // 2, (w + 1) // 2))
+    return dims
+
+
+def algorithmic_bytes(kind, level, dims, K, frames, levels):
+    """Minimal HBM bytes one launch must move."""
+    N = lambda l: dims[l][0] * dims[l][1]  # noqa: E731
+    lmax = levels - 1
+    if kind == "build0":
+        b = 4 * N(0) + (4 + 8 * K) * N(1)
+    elif kind == "build":
+        b = (4 + 8 * K) * (N(level) + N(level + 1))
+    elif kind == "apply0":
+        has_d = 1 < lmax
+        b = 8 * N(0) + (8 * K + (4 if has_d else 0)) * N(1)
+    elif kind == "apply":
+        has_d = level + 1 < lmax
+        b = (8 + 8 * K) * N(level) + (8 * K + (4 if has_d else 0)) * N(level + 1)
+    else:
+        b = 0
+    return b * frames
+
+
+# ------------------------------------------------------------ CPU baseline
+def cpu_baseline(img, c, budget_s=12.0, max_frames=3):
+    """The oracle as it stands (numpy fp64), on full frames of the workload."""
+    from oracle import fllf_oracle as O
+    n, t0 = 0, time.perf_counter()
+    while n < max_frames:
+        O.fourier_llf(img.astype(np.float64), c["levels"], c["K"], c["T"], c["sigma_r"], c["m"])
+        n += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    H, W = img.shape
+    return {"value": round(n * H * W / 1e6 / dt, 4), "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{n} full {H}x{W} frame(s) of the workload through oracle/fllf_oracle.py "
+                      f"(numpy fp64, single-threaded), {dt:.1f} s"}
+
+
+# --------------------------------------------------------------- reference
+def run_reference(args):
+    """--impl reference: the oracle timed on host cores on a bounded sample of
+    the same workload (a 270x480 crop = 1/16 of a config-2 frame per step)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import fllf_oracle as O
+    from paper_2206_04681_b200 import synth
+    wl = WORKLOADS[args.workload]
+    c = synth.CONFIGS[wl["cfg"]]
+    img = synth.config2_image(seed=2000 if wl["cfg"] == 2 else 5000)[:270, :480].astype(np.float64)
+    for _ in range(args.warmup):
+        O.fourier_llf(img, c["levels"], c["K"], c["T"], c["sigma_r"], c["m"])
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.fourier_llf(img, c["levels"], c["K"], c["T"], c["sigma_r"], c["m"])
+    dt = time.perf_counter() - t0
+    v = args.steps * img.size / 1e6 / dt
+    sample = f"270x480 crop (1/16 of a 1080x1920 frame) of the {args.workload} workload per step"
+    line = {"metric": METRIC, "value": round(v, 4), "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * dt / args.steps, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": wl["desc"], "sample": sample},
+            "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": round(v, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["fllf", "reference"], default="fllf")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="config2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2206_04681_b200 import fllf as F
+    from paper_2206_04681_b200 import synth
+
+    wl = WORKLOADS[args.workload]
+    c = synth.CONFIGS[wl["cfg"]]
+    H, W, levels, K = c["H"], c["W"], c["levels"], c["K"]
+    if wl["cfg"] == 2:
+        frames = 1
+        imgs = np.stack([synth.config2_image(seed=2000 + rank)])
+        scaling = "weak"
+    else:
+        total = wl["frames"]
+        frames = total // world
+        first = rank * frames
+        imgs = synth.config5_frames(frames, first=first)
+        scaling = "strong"
+    stream = torch.cuda.current_stream()
+    d_in = torch.from_numpy(imgs).cuda()
+    d_out = torch.empty_like(d_in)
+    props = torch.cuda.get_device_properties(local)
+    l2 = getattr(props, "L2_cache_size", 126 * 2 ** 20) or 126 * 2 ** 20
+    flush_buf = torch.empty(2 * l2 // 4 + 1024, dtype=torch.float32, device="cuda")
+
+    def flush():
+        flush_buf.zero_()
+
+    plan = F.Plan(H, W, levels, K, c["T"], c["sigma_r"], c["m"], batch=frames)
+    F.fllf_plan_set_profiling(plan.handle, True)
+    for _ in range(max(args.warmup, 0)):
+        flush()
+        plan.filter(d_in, d_out, stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    clk = ClockSampler(local)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    per_kernel = {}
+    launches = 0
+    torch.cuda.synchronize()
+    clk.start()
+    for i in range(args.steps):
+        flush()
+        starts[i].record(stream)
+        plan.filter(d_in, d_out, stream)
+        ends[i].record(stream)
+        launches += plan.launches
+        for kind, lev, ms in F.fllf_plan_kernel_times(plan.handle):
+            per_kernel.setdefault((kind, lev), []).append(ms)
+    torch.cuda.synchronize()
+    clk.stop()
+    if world > 1:
+        dist.barrier()
+    my_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    t = torch.tensor([my_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tot_ms = float(t.item())
+    px = world * frames * H * W * args.steps
+    value = px / 1e6 / (tot_ms / 1e3)
+
+    # ---- per-kernel table, dominant kernel, roofline
+    dims = level_dims(H, W, levels)
+    peak, peak_src = hbm_peak()
+    rows = []
+    for (kind, lev), v in per_kernel.items():
+        avg = sum(v) / len(v)
+        b = algorithmic_bytes(kind, lev, dims, K, frames, levels)
+        rows.append((sum(v), kind, lev, avg, b))
+    rows.sort(reverse=True)
+    step_kernel_ms = sum(r[0] for r in rows) / args.steps
+    for tot, kind, lev, avg, b in rows:
+        log(f"[bench] {kind:7s} l={lev}  avg {avg * 1e3:8.2f} us  share {tot / args.steps / step_kernel_ms:5.1%}"
+            f"  alg {b / 1e6:8.2f} MB  {b / (avg * 1e-3) / 1e9:8.1f} GB/s")
+    dom = rows[0]
+    achieved = dom[4] / (dom[3] * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+    if os.path.exists(tp):
+        try:
+            tj = json.load(open(tp))
+            key = f"{args.workload}:{dom[1]}:{dom[2]}"
+            traffic = tj.get(key)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "kernel": f"{dom[1]} (level {dom[2]})", "achieved": round(achieved, 1),
+                "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                "alg_bytes_per_launch": dom[4], "avg_launch_us": round(dom[3] * 1e3, 2),
+                "share_of_step": round(dom[0] / args.steps / step_kernel_ms, 3), "peak_source": peak_src}
+
+    # ---- end to end through the C ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        h_in = torch.from_numpy(imgs.copy()).pin_memory()
+        h_out = torch.empty_like(h_in).pin_memory()
+        for _ in range(2):
+            F.fllf_filter_host(plan.handle, h_in, h_out, stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        es = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        clk.start()
+        for a, b in es:
+            flush()
+            a.record(stream)
+            F.fllf_filter_host(plan.handle, h_in, h_out, stream)
+            b.record(stream)
+        torch.cuda.synchronize()
+        clk.stop()
+        e_ms = torch.tensor([sum(a.elapsed_time(b) for a, b in es)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        nbytes = frames * H * W * 4
+        e2e = {"value": round(px / 1e6 / (float(e_ms.item()) / 1e3), 2), "unit": UNIT,
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+               "api": "fllf_filter_host (pinned host buffers, H2D + build + apply + D2H)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(imgs[0], c)
+    clk.close()
+    plan.close()
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot_ms / args.steps, 4),
+                "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic",
+                "config": {"workload": wl["desc"], "frames_per_rank": frames, "H": H, "W": W,
+                           "levels": levels, "K": K, "T": c["T"], "sigma_r": c["sigma_r"], "m": c["m"],
+                           "parallelism": f"frame-dp{world}" if world > 1 else "single",
+                           "l2": f"flushed between timed steps ({flush_buf.numel() * 4 >> 20} MiB write)"},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,176 @@
+/*
+ * libfllf -- B200-native Fourier local Laplacian filtering (C ABI).
+ *
+ * Implements the data-parallel hot path of "Gaussian Fourier Pyramid for
+ * Local Laplacian Filter" (Sumiya, Otsuka, Maeda, Fukushima, arXiv 2206.04681).
+ * Citations "P:n" are lines of the paper's text, given with the
+ * section / equation they fall in.
+ *
+ * What is computed:
+ *   omega_k = 2 pi k / T,  alpha_k = sigma_r sqrt(2 pi)/T exp(-(omega_k sigma_r)^2/2),
+ *   alpha~_k = 2 sigma_r^2 alpha_k omega_k,  a_k = m alpha~_k     (Eq. 9-11)
+ *   G_l = Gaussian pyramid of I (Eq. 1),
+ *   Z_{l,k} = C~_{l,k} + i S~_{l,k} = G_l[cos w_k I] + i G_l[sin w_k I]
+ *   L_l[O] = L_l[I] + sum_k a_k ( cos(w_k g) L_l[S~_k] - sin(w_k g) L_l[C~_k] ),
+ *            g = G_l[I] pointwise, l < l_max;  L_lmax[O] = G_lmax[I]    (Eq. 14)
+ *   O = collapse(L[O])                                                   (Eq. 4,  P:138-141)
+ * with the enhancing remap sign r(i,g) = i + m (i-g) exp(-(i-g)^2/(2 sigma_r^2))
+ * (reading R1).  Borders are reflect-101, sizes halve with ceil, the
+ * up-sampling kernel is 2x the 5-tap binomial per axis (readings R2, R3, R5).
+ *
+ * Conventions for every entry point:
+ *   - Images are fp32, row-major: pixel (x, y) of frame f lives at
+ *     (char*)base + f*H*pitch_bytes + y*pitch_bytes + 4*x.  pitch_bytes = 0
+ *     means W*4.  pitch_bytes must be >= W*4 and a multiple of 4.
+ *   - Pointers prefixed d_ are DEVICE pointers on the plan's device; h_ are
+ *     HOST pointers (pinned memory makes the copies asynchronous).
+ *   - All work is enqueued asynchronously on the caller's stream `s`
+ *     (a cudaStream_t; NULL = legacy default stream).  The caller keeps every
+ *     buffer alive until that stream work has completed.
+ *   - A plan owns all device workspace (the pyramids); it is bound to one
+ *     device, is not thread-safe, and may be used by one stream at a time.
+ *     Distinct plans may run concurrently on distinct streams.
+ *   - No C++ exception crosses this boundary.  On failure the status code is
+ *     returned and fllf_last_error_message() (thread-local) holds the detail;
+ *     CUDA failures return FLLF_ERR_CUDA.
+ *   - There is no CPU fallback: without a CUDA device every compute entry
+ *     point returns FLLF_ERR_CUDA.
+ */
+#ifndef FLLF_H_
+#define FLLF_H_
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define FLLF_API __attribute__((visibility("default")))
+#else
+#define FLLF_API
+#endif
+
+#define FLLF_MAX_K 32      /* maximum Fourier order K (2K+1 pyramids)          */
+#define FLLF_MAX_LEVELS 16 /* maximum pyramid levels                            */
+
+typedef struct fllf_plan_s* fllf_plan; /* opaque; owns the device workspace */
+
+typedef enum {
+  FLLF_OK = 0,
+  FLLF_ERR_INVALID_ARGUMENT = 1, /* H,W<1; levels<2; K<1 or >FLLF_MAX_K; T<=0; sigma_r<=0;
+                                    non-finite value; bad order range; batch<1         */
+  FLLF_ERR_TOO_MANY_LEVELS = 2,  /* a dimension of the coarsest level would be < 3, or
+                                    levels > FLLF_MAX_LEVELS                            */
+  FLLF_ERR_OUT_OF_MEMORY = 3,    /* workspace allocation failed                         */
+  FLLF_ERR_CUDA = 4,             /* a CUDA runtime call or kernel launch failed         */
+  FLLF_ERR_NOT_BUILT = 5,        /* fllf_apply before fllf_build_fourier_pyramids       */
+  FLLF_ERR_BAD_POINTER = 6,      /* NULL pointer, pitch < W*4 or not a multiple of 4    */
+} fllf_status;
+
+typedef enum {
+  FLLF_SCALAR = 0, /* a_k = m alpha~_k from the plan's (sigma_r, m)   (Eq. 11)     */
+  FLLF_COEFFS = 1, /* caller-given a_k, k = k_begin..k_end-1: any remap whose detail term
+                      is odd in (i-g) with period T ("change the function by
+                      switching only the coefficient")                                  */
+  FLLF_MAPS = 2    /* per-pixel sigma_r(p), m(p) (Sec. III-B); at level l
+                      the maps' Gaussian pyramids are used (reading R7)                 */
+} fllf_apply_mode;
+
+/* Full plan description (fllf_plan_create fills the defaults shown). */
+typedef struct {
+  int H, W;         /* frame size (pixels)                                             */
+  int levels;       /* pyramid levels incl. the residual, >= 2 (l_max = levels-1) */
+  int K;            /* Fourier order, 1..FLLF_MAX_K                                      */
+  double T;         /* period of the expansion (Eq. 9)                        */
+  double sigma_r;   /* remap range scale (Eq. 6)                                  */
+  double m;         /* remap gain (Eq. 6; m > 0 enhances)                         */
+  int batch;        /* frames per call, >= 1 (default 1); frames are contiguous          */
+  int k_begin;      /* order range [k_begin, k_end), 1 <= k_begin < k_end <= K+1;        */
+  int k_end;        /*   0,0 = all orders (default).  Order sharding across GPUs.        */
+  int include_base; /* 1 (default): output = full O.  0: output = the partial collapse of
+                       the range's Fourier terms only (no L[I], top level 0); summing the
+                       partials of a partition of 1..K and adding I gives O (Eq. 4 is
+                       linear).                                                           */
+  int device;       /* CUDA device ordinal; -1 (default) = the current device            */
+} fllf_plan_desc;
+
+/* Per-apply arguments; NULL means FLLF_SCALAR. */
+typedef struct {
+  int mode;                /* fllf_apply_mode                                            */
+  const double* a_k;       /* COEFFS: HOST array of (k_end - k_begin) values              */
+  const float* d_sigma_r;  /* MAPS: DEVICE full-resolution sigma_r map (> 0), H x W      */
+  const float* d_m;        /* MAPS: DEVICE full-resolution m map, H x W                  */
+  size_t map_pitch_bytes;  /* MAPS: pitch of both maps (0 = W*4); maps are shared by all
+                              frames of a batch                                           */
+} fllf_apply_args;
+
+/* Create a plan for H x W frames: validates the arguments (see fllf_status),
+ * computes the level sizes (ceil-halving), allocates the pyramid workspace on
+ * the device and converts the fp64 coefficients to fp32. */
+FLLF_API fllf_status fllf_plan_create(int H, int W, int levels, int K, double T, double sigma_r,
+                             double m, fllf_plan* out);
+FLLF_API fllf_status fllf_plan_create_ex(const fllf_plan_desc* d, fllf_plan* out);
+
+/* Destroy a plan and free its workspace.  NULL-safe; synchronises the device. */
+FLLF_API fllf_status fllf_destroy(fllf_plan p);
+
+/* Build the 2K+1 pyramids of P:262 for levels 1..l_max from d_img (batch
+ * frames): G_l[I] and Z_{l,k} for the plan's order range.  Level 0 of the
+ * Fourier pyramids is never stored: cos/sin(omega_k I) are formed on the fly
+ * inside the first blur-and-decimate (north star; P:250 shows level 0 needs
+ * only the up-sampled level-1 terms). */
+FLLF_API fllf_status fllf_build_fourier_pyramids(fllf_plan p, const float* d_img, size_t pitch_bytes,
+                                        void* s);
+
+/* Product-sum + collapse (Eq. 14 + Eq. 4) from the pyramids of the most recent
+ * build on this plan; writes O (or the partial output, include_base = 0) to
+ * d_out.  `a` = NULL selects FLLF_SCALAR.  May be called many times per build
+ * with different coefficients or maps.  Reads d_img of
+ * that build again (level 0 needs I): the caller keeps it alive and unchanged. */
+FLLF_API fllf_status fllf_apply(fllf_plan p, const fllf_apply_args* a, float* d_out,
+                       size_t out_pitch_bytes, void* s);
+
+/* build + apply(SCALAR) in one call (the common one-shot filter). */
+FLLF_API fllf_status fllf_filter(fllf_plan p, const float* d_img, size_t in_pitch_bytes, float* d_out,
+                        size_t out_pitch_bytes, void* s);
+
+/* End-to-end from HOST memory: copies the batch h_img -> device staging,
+ * build, apply(SCALAR), copies the result -> h_out (dense W*4 pitch both).
+ * Asynchronous on `s` (pinned host memory); synchronise `s` before reading h_out. */
+FLLF_API fllf_status fllf_filter_host(fllf_plan p, const float* h_img, float* h_out, void* s);
+
+/* Host helper: omega_k and a_k = m alpha~_k for k = 1..K in fp64 (Eq. 9-11). */
+FLLF_API fllf_status fllf_coefficients(int K, double T, double sigma_r, double m, double* omega_out,
+                              double* a_out);
+
+/* Introspection (tests, tooling). */
+FLLF_API fllf_status fllf_plan_level_dims(fllf_plan p, int level, int* H, int* W);
+FLLF_API fllf_status fllf_workspace_bytes(fllf_plan p, size_t* bytes);
+/* Copy one built pyramid plane (levels 1..l_max) of one frame to d_dst:
+ * channel 0 = G_l[I] (H_l x W_l floats); channel c = 1..(k_end-k_begin) =
+ * Z_{l, k_begin+c-1} as interleaved (S~, C~) float pairs (H_l x 2W_l floats). */
+FLLF_API fllf_status fllf_read_pyramid(fllf_plan p, int frame, int level, int channel, float* d_dst,
+                              size_t dst_pitch_bytes, void* s);
+
+/* Kernels launched by the most recent build / apply / filter call of this plan. */
+FLLF_API int fllf_plan_last_launch_count(fllf_plan p);
+
+/* Per-kernel timing (bench tooling).  With profiling enabled every kernel
+ * launch is bracketed by two CUDA events recorded on the launch stream.  The
+ * record list restarts at each build (and at an apply that follows an apply).
+ * fllf_plan_kernel_times synchronises those events and returns, per launch in
+ * order: kind (FLLF_K_*), pyramid level (the fine level of the step) and the
+ * duration in milliseconds; *count = number of records (<= capacity). */
+enum { FLLF_K_BUILD0 = 0, FLLF_K_BUILD = 1, FLLF_K_MAPBUILD = 2, FLLF_K_APPLY = 3, FLLF_K_APPLY0 = 4 };
+FLLF_API fllf_status fllf_plan_set_profiling(fllf_plan p, int enable);
+FLLF_API fllf_status fllf_plan_kernel_times(fllf_plan p, int capacity, int* kind, int* level,
+                                            float* ms, int* count);
+
+FLLF_API const char* fllf_status_string(fllf_status st);
+FLLF_API const char* fllf_last_error_message(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLLF_H_ */

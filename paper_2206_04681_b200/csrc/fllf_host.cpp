@@ -1,0 +1,546 @@
+// libfllf C ABI: plan creation, workspace layout, fp64 coefficient math and
+// launch sequencing (DESIGN.md "Boundary" and "Data layout in HBM").
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "fllf.h"
+#include "fllf_internal.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+fllf_status fail(fllf_status st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
+
+fllf_status cuda_fail(cudaError_t e, const char* what) {
+  g_last_error = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+  return FLLF_ERR_CUDA;
+}
+
+constexpr double kPi = 3.14159265358979323846;
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// Scoped switch to the plan's device.
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) {
+      ok = false;
+      return;
+    }
+    if (dev >= 0 && dev != prev) ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+bool is_finite(double v) { return std::isfinite(v); }
+
+}  // namespace
+
+struct fllf_plan_s {
+  fllf_plan_desc d{};
+  int KL = 0;          // local orders
+  int kb = 1;          // first global order
+  int device = 0;
+  int nlev = 0;
+  int Hs[FLLF_MAX_LEVELS]{}, Ws[FLLF_MAX_LEVELS]{};
+  fllf::DevLevel lv[FLLF_MAX_LEVELS]{};
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  void* maps_ws = nullptr;
+  bool built = false;
+  const float* img = nullptr;  // the image of the most recent build
+  long long img_pitch = 0;     // floats
+  float* stage_in = nullptr;
+  float* stage_out = nullptr;
+  int last_launches = 0;
+  // profiling: one (start, stop) event pair per launch record
+  bool profiling = false;
+  bool last_was_apply = false;
+  std::vector<cudaEvent_t> ev_start, ev_stop;
+  std::vector<int> rec_kind, rec_level;
+  int nrec = 0;
+};
+
+namespace {
+// Bracket one launch with profiling events (no-op when profiling is off).
+struct ProfScope {
+  fllf_plan p;
+  cudaStream_t s;
+  int idx = -1;
+  ProfScope(fllf_plan p_, cudaStream_t s_, int kind, int level) : p(p_), s(s_) {
+    if (!p->profiling) return;
+    idx = p->nrec++;
+    if ((int)p->ev_start.size() <= idx) {
+      cudaEvent_t a, b;
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      p->ev_start.push_back(a);
+      p->ev_stop.push_back(b);
+      p->rec_kind.push_back(0);
+      p->rec_level.push_back(0);
+    }
+    p->rec_kind[idx] = kind;
+    p->rec_level[idx] = level;
+    cudaEventRecord(p->ev_start[idx], s);
+  }
+  ~ProfScope() {
+    if (idx >= 0) cudaEventRecord(p->ev_stop[idx], s);
+  }
+};
+}  // namespace
+
+extern "C" {
+
+const char* fllf_status_string(fllf_status st) {
+  switch (st) {
+    case FLLF_OK: return "FLLF_OK";
+    case FLLF_ERR_INVALID_ARGUMENT: return "FLLF_ERR_INVALID_ARGUMENT";
+    case FLLF_ERR_TOO_MANY_LEVELS: return "FLLF_ERR_TOO_MANY_LEVELS";
+    case FLLF_ERR_OUT_OF_MEMORY: return "FLLF_ERR_OUT_OF_MEMORY";
+    case FLLF_ERR_CUDA: return "FLLF_ERR_CUDA";
+    case FLLF_ERR_NOT_BUILT: return "FLLF_ERR_NOT_BUILT";
+    case FLLF_ERR_BAD_POINTER: return "FLLF_ERR_BAD_POINTER";
+  }
+  return "FLLF_ERR_UNKNOWN";
+}
+
+const char* fllf_last_error_message(void) { return g_last_error.c_str(); }
+
+// Eq. 9-11: omega_k = 2 pi k/T, alpha_k = sigma sqrt(2 pi)/T
+// exp(-(omega_k sigma)^2/2), a_k = m * 2 sigma^2 alpha_k omega_k.
+fllf_status fllf_coefficients(int K, double T, double sigma_r, double m, double* omega_out,
+                              double* a_out) {
+  if (K < 1 || !(T > 0) || !(sigma_r > 0) || !is_finite(T) || !is_finite(sigma_r) || !is_finite(m))
+    return fail(FLLF_ERR_INVALID_ARGUMENT, "fllf_coefficients: need K>=1, T>0, sigma_r>0, finite m");
+  if (!omega_out && !a_out) return fail(FLLF_ERR_BAD_POINTER, "fllf_coefficients: no output array");
+  for (int k = 1; k <= K; ++k) {
+    const double w = 2.0 * kPi * k / T;
+    const double alpha = sigma_r * std::sqrt(2.0 * kPi) / T * std::exp(-0.5 * (w * sigma_r) * (w * sigma_r));
+    if (omega_out) omega_out[k - 1] = w;
+    if (a_out) a_out[k - 1] = m * 2.0 * sigma_r * sigma_r * alpha * w;
+  }
+  return FLLF_OK;
+}
+
+fllf_status fllf_plan_create(int H, int W, int levels, int K, double T, double sigma_r, double m,
+                             fllf_plan* out) {
+  fllf_plan_desc d{};
+  d.H = H; d.W = W; d.levels = levels; d.K = K; d.T = T; d.sigma_r = sigma_r; d.m = m;
+  d.batch = 1; d.k_begin = 0; d.k_end = 0; d.include_base = 1; d.device = -1;
+  return fllf_plan_create_ex(&d, out);
+}
+
+fllf_status fllf_plan_create_ex(const fllf_plan_desc* din, fllf_plan* out) {
+  if (!din || !out) return fail(FLLF_ERR_BAD_POINTER, "fllf_plan_create: NULL argument");
+  *out = nullptr;
+  fllf_plan_desc d = *din;
+  if (d.H < 1 || d.W < 1) return fail(FLLF_ERR_INVALID_ARGUMENT, "H and W must be >= 1");
+  if (d.levels < 2) return fail(FLLF_ERR_INVALID_ARGUMENT, "levels must be >= 2");
+  if (d.K < 1 || d.K > FLLF_MAX_K) return fail(FLLF_ERR_INVALID_ARGUMENT, "K must be in 1..32");
+  if (!is_finite(d.T) || !(d.T > 0)) return fail(FLLF_ERR_INVALID_ARGUMENT, "T must be finite and > 0");
+  if (!is_finite(d.sigma_r) || !(d.sigma_r > 0))
+    return fail(FLLF_ERR_INVALID_ARGUMENT, "sigma_r must be finite and > 0");
+  if (!is_finite(d.m)) return fail(FLLF_ERR_INVALID_ARGUMENT, "m must be finite");
+  if (d.batch < 1) return fail(FLLF_ERR_INVALID_ARGUMENT, "batch must be >= 1");
+  if (d.k_begin == 0 && d.k_end == 0) {
+    d.k_begin = 1;
+    d.k_end = d.K + 1;
+  }
+  if (d.k_begin < 1 || d.k_end <= d.k_begin || d.k_end > d.K + 1)
+    return fail(FLLF_ERR_INVALID_ARGUMENT, "order range must satisfy 1 <= k_begin < k_end <= K+1");
+  if (d.levels > FLLF_MAX_LEVELS) return fail(FLLF_ERR_TOO_MANY_LEVELS, "levels > FLLF_MAX_LEVELS");
+  int h = d.H, w = d.W;
+  for (int l = 1; l < d.levels; ++l) {
+    h = (h + 1) / 2;
+    w = (w + 1) / 2;
+  }
+  if (h < 3 || w < 3)
+    return fail(FLLF_ERR_TOO_MANY_LEVELS, "coarsest level would be smaller than 3x3 (" + std::to_string(h) +
+                                              "x" + std::to_string(w) + ")");
+
+  fllf_plan p = new (std::nothrow) fllf_plan_s();
+  if (!p) return fail(FLLF_ERR_OUT_OF_MEMORY, "host allocation failed");
+  p->d = d;
+  p->KL = d.k_end - d.k_begin;
+  p->kb = d.k_begin;
+  p->nlev = d.levels;
+  int dev = d.device;
+  if (dev < 0) {
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+      delete p;
+      cudaGetLastError();
+      return fail(FLLF_ERR_CUDA, "no CUDA device available (libfllf has no CPU fallback)");
+    }
+  }
+  p->device = dev;
+  DeviceGuard guard(dev);
+  if (!guard.ok) {
+    delete p;
+    cudaGetLastError();
+    return fail(FLLF_ERR_CUDA, "cannot select CUDA device " + std::to_string(dev));
+  }
+
+  p->Hs[0] = d.H;
+  p->Ws[0] = d.W;
+  for (int l = 1; l < d.levels; ++l) {
+    p->Hs[l] = (p->Hs[l - 1] + 1) / 2;
+    p->Ws[l] = (p->Ws[l - 1] + 1) / 2;
+  }
+  // workspace layout: per level l >= 1: G | D | Z  (each 256-byte aligned)
+  const size_t B = (size_t)d.batch;
+  size_t off = 0;
+  std::vector<size_t> offG(d.levels), offD(d.levels), offZ(d.levels);
+  for (int l = 1; l < d.levels; ++l) {
+    const size_t pitch_r = align_up((size_t)p->Ws[l], 32);  // floats (128 B)
+    const size_t pitch_c = align_up((size_t)p->Ws[l], 16);  // float2 (128 B)
+    // one pitch value serves both kinds: use the float2 pitch rounded to 32
+    const size_t pitch = std::max(pitch_r, align_up(pitch_c, 32));
+    fllf::DevLevel& L = p->lv[l];
+    L.H = p->Hs[l];
+    L.W = p->Ws[l];
+    L.pitch = (int)pitch;
+    L.fstride_r = (long long)(L.H * pitch);
+    L.kstride_z = (long long)(L.H * pitch);
+    L.fstride_z = (long long)p->KL * L.kstride_z;
+    offG[l] = off;
+    off = align_up(off + B * L.fstride_r * sizeof(float), 256);
+    offD[l] = off;
+    off = align_up(off + B * L.fstride_r * sizeof(float), 256);
+    offZ[l] = off;
+    off = align_up(off + B * (size_t)L.fstride_z * sizeof(float2), 256);
+  }
+  p->ws_bytes = off;
+  cudaError_t e = cudaMalloc(&p->ws, off);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    delete p;
+    return e == cudaErrorMemoryAllocation
+               ? fail(FLLF_ERR_OUT_OF_MEMORY, "workspace cudaMalloc of " + std::to_string(off) + " bytes failed")
+               : cuda_fail(e, "cudaMalloc");
+  }
+  char* base = static_cast<char*>(p->ws);
+  for (int l = 1; l < d.levels; ++l) {
+    p->lv[l].G = reinterpret_cast<float*>(base + offG[l]);
+    p->lv[l].D = reinterpret_cast<float*>(base + offD[l]);
+    p->lv[l].Z = reinterpret_cast<float2*>(base + offZ[l]);
+  }
+  *out = p;
+  return FLLF_OK;
+}
+
+fllf_status fllf_destroy(fllf_plan p) {
+  if (!p) return FLLF_OK;
+  {
+    DeviceGuard guard(p->device);
+    cudaDeviceSynchronize();
+    if (p->ws) cudaFree(p->ws);
+    if (p->maps_ws) cudaFree(p->maps_ws);
+    if (p->stage_in) cudaFree(p->stage_in);
+    if (p->stage_out) cudaFree(p->stage_out);
+    for (cudaEvent_t e : p->ev_start) cudaEventDestroy(e);
+    for (cudaEvent_t e : p->ev_stop) cudaEventDestroy(e);
+    cudaGetLastError();
+  }
+  delete p;
+  return FLLF_OK;
+}
+
+static fllf_status check_image(const void* ptr, size_t pitch_bytes, int W, const char* what,
+                               long long* pitch_floats) {
+  if (!ptr) return fail(FLLF_ERR_BAD_POINTER, std::string(what) + ": NULL pointer");
+  if (pitch_bytes == 0) pitch_bytes = (size_t)W * 4;
+  if (pitch_bytes < (size_t)W * 4 || (pitch_bytes & 3))
+    return fail(FLLF_ERR_BAD_POINTER, std::string(what) + ": pitch must be >= W*4 and a multiple of 4");
+  if (reinterpret_cast<uintptr_t>(ptr) & 3)
+    return fail(FLLF_ERR_BAD_POINTER, std::string(what) + ": pointer not 4-byte aligned");
+  *pitch_floats = (long long)(pitch_bytes / 4);
+  return FLLF_OK;
+}
+
+fllf_status fllf_build_fourier_pyramids(fllf_plan p, const float* d_img, size_t pitch_bytes, void* s) {
+  if (!p) return fail(FLLF_ERR_BAD_POINTER, "NULL plan");
+  long long pitch;
+  fllf_status st = check_image(d_img, pitch_bytes, p->d.W, "build: d_img", &pitch);
+  if (st != FLLF_OK) return st;
+  DeviceGuard guard(p->device);
+  cudaStream_t stream = static_cast<cudaStream_t>(s);
+  const double T = p->d.T;
+  int launches = 0;
+  p->nrec = 0;
+  p->last_was_apply = false;
+  for (int l = 0; l + 1 < p->nlev; ++l) {
+    fllf::BuildParams bp{};
+    bp.img.p = d_img;
+    bp.img.H = p->d.H;
+    bp.img.W = p->d.W;
+    bp.img.pitch = pitch;
+    bp.img.fstride = pitch * p->d.H;
+    if (l > 0) bp.src = p->lv[l];
+    bp.dst = p->lv[l + 1];
+    bp.Hf = p->Hs[l];
+    bp.Wf = p->Ws[l];
+    bp.Hc = p->Hs[l + 1];
+    bp.Wc = p->Ws[l + 1];
+    bp.KL = p->KL;
+    bp.kbase = p->kb;
+    bp.maps = 0;
+    bp.invT = (float)(1.0 / T);
+    cudaError_t e;
+    {
+      ProfScope ps(p, stream, l == 0 ? FLLF_K_BUILD0 : FLLF_K_BUILD, l);
+      e = fllf::launch_build(bp, l, p->d.batch, stream);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "build kernel launch");
+    ++launches;
+  }
+  p->built = true;
+  p->img = d_img;
+  p->img_pitch = pitch;
+  p->last_launches = launches;
+  return FLLF_OK;
+}
+
+static fllf_status ensure_maps_ws(fllf_plan p) {
+  if (p->maps_ws) return FLLF_OK;
+  size_t off = 0;
+  std::vector<size_t> offs(p->nlev);
+  for (int l = 1; l < p->nlev; ++l) {
+    offs[l] = off;
+    off = align_up(off + 2 * (size_t)p->lv[l].fstride_r * sizeof(float), 256);
+  }
+  cudaError_t e = cudaMalloc(&p->maps_ws, off);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(FLLF_ERR_OUT_OF_MEMORY, "map pyramid cudaMalloc failed");
+  }
+  char* base = static_cast<char*>(p->maps_ws);
+  for (int l = 1; l < p->nlev; ++l) {
+    p->lv[l].MS = reinterpret_cast<float*>(base + offs[l]);
+    p->lv[l].MM = p->lv[l].MS + p->lv[l].fstride_r;
+  }
+  return FLLF_OK;
+}
+
+fllf_status fllf_apply(fllf_plan p, const fllf_apply_args* a, float* d_out, size_t out_pitch_bytes, void* s) {
+  if (!p) return fail(FLLF_ERR_BAD_POINTER, "NULL plan");
+  if (!p->built) return fail(FLLF_ERR_NOT_BUILT, "fllf_apply before fllf_build_fourier_pyramids");
+  long long opitch;
+  fllf_status st = check_image(d_out, out_pitch_bytes, p->d.W, "apply: d_out", &opitch);
+  if (st != FLLF_OK) return st;
+  const int mode = a ? a->mode : FLLF_SCALAR;
+  if (mode != FLLF_SCALAR && mode != FLLF_COEFFS && mode != FLLF_MAPS)
+    return fail(FLLF_ERR_INVALID_ARGUMENT, "apply: unknown mode");
+  DeviceGuard guard(p->device);
+  cudaStream_t stream = static_cast<cudaStream_t>(s);
+  const double T = p->d.T;
+  const double w1 = 2.0 * kPi / T;
+
+  fllf::ApplyParams ap{};
+  ap.img.p = p->img;
+  ap.img.H = p->d.H;
+  ap.img.W = p->d.W;
+  ap.img.pitch = p->img_pitch;
+  ap.img.fstride = p->img_pitch * p->d.H;
+  ap.out = d_out;
+  ap.out_pitch = opitch;
+  ap.out_fstride = opitch * p->d.H;
+  ap.KL = p->KL;
+  ap.kbase = p->kb;
+  ap.include_base = p->d.include_base;
+  ap.invT = (float)(1.0 / T);
+  ap.c0 = (float)(2.0 * w1 * std::sqrt(2.0 * kPi) / T);
+  ap.hq = (float)(0.5 * w1 * w1);
+
+  if (mode == FLLF_SCALAR || mode == FLLF_COEFFS) {
+    std::vector<double> om(p->d.K), ak(p->d.K);
+    if (mode == FLLF_SCALAR) {
+      fllf_coefficients(p->d.K, T, p->d.sigma_r, p->d.m, om.data(), ak.data());
+      for (int i = 0; i < p->KL; ++i) ap.a[i] = (float)ak[p->kb - 1 + i];
+    } else {
+      if (!a->a_k) return fail(FLLF_ERR_BAD_POINTER, "apply(COEFFS): a_k is NULL");
+      for (int i = 0; i < p->KL; ++i) {
+        if (!is_finite(a->a_k[i])) return fail(FLLF_ERR_INVALID_ARGUMENT, "apply(COEFFS): non-finite a_k");
+        ap.a[i] = (float)a->a_k[i];
+      }
+    }
+  }
+  int launches = 0;
+  if (p->last_was_apply) p->nrec = 0;
+  p->last_was_apply = true;
+  const bool maps = mode == FLLF_MAPS;
+  if (maps) {
+    long long mp1, mp2;
+    st = check_image(a->d_sigma_r, a->map_pitch_bytes, p->d.W, "apply(MAPS): d_sigma_r", &mp1);
+    if (st != FLLF_OK) return st;
+    st = check_image(a->d_m, a->map_pitch_bytes, p->d.W, "apply(MAPS): d_m", &mp2);
+    if (st != FLLF_OK) return st;
+    st = ensure_maps_ws(p);
+    if (st != FLLF_OK) return st;
+    ap.smap.p = a->d_sigma_r;
+    ap.smap.pitch = mp1;
+    ap.mmap.p = a->d_m;
+    ap.mmap.pitch = mp2;
+    // Gaussian pyramids of the two maps, levels 1 .. l_max-1 (reading R7)
+    for (int l = 0; l + 2 < p->nlev; ++l) {
+      fllf::BuildParams bp{};
+      bp.img.p = a->d_sigma_r;
+      bp.img.pitch = mp1;
+      bp.img.fstride = 0;
+      bp.img2.p = a->d_m;
+      bp.img2.pitch = mp2;
+      bp.img2.fstride = 0;
+      if (l > 0) bp.src = p->lv[l];
+      bp.dst = p->lv[l + 1];
+      bp.Hf = p->Hs[l];
+      bp.Wf = p->Ws[l];
+      bp.Hc = p->Hs[l + 1];
+      bp.Wc = p->Ws[l + 1];
+      bp.KL = 0;
+      bp.kbase = p->kb;
+      bp.maps = 1;
+      bp.invT = (float)(1.0 / T);
+      cudaError_t e;
+      {
+        ProfScope ps(p, stream, FLLF_K_MAPBUILD, l);
+        e = fllf::launch_build(bp, l, 1, stream);
+      }
+      if (e != cudaSuccess) return cuda_fail(e, "map pyramid kernel launch");
+      ++launches;
+    }
+  }
+  const int lmax = p->nlev - 1;
+  for (int l = lmax - 1; l >= 0; --l) {
+    if (l > 0) ap.fine = p->lv[l];
+    ap.coarse = p->lv[l + 1];
+    ap.Hf = p->Hs[l];
+    ap.Wf = p->Ws[l];
+    ap.Hc = p->Hs[l + 1];
+    ap.Wc = p->Ws[l + 1];
+    const bool has_d = (l + 1) < lmax;  // D_lmax = 0
+    cudaError_t e;
+    {
+      ProfScope ps(p, stream, l == 0 ? FLLF_K_APPLY0 : FLLF_K_APPLY, l);
+      e = fllf::launch_apply(ap, l, has_d, maps, p->d.batch, stream);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "apply kernel launch");
+    ++launches;
+  }
+  p->last_launches = launches;
+  return FLLF_OK;
+}
+
+fllf_status fllf_filter(fllf_plan p, const float* d_img, size_t in_pitch_bytes, float* d_out,
+                        size_t out_pitch_bytes, void* s) {
+  fllf_status st = fllf_build_fourier_pyramids(p, d_img, in_pitch_bytes, s);
+  if (st != FLLF_OK) return st;
+  const int nb = p->last_launches;
+  st = fllf_apply(p, nullptr, d_out, out_pitch_bytes, s);
+  if (st == FLLF_OK) p->last_launches += nb;
+  return st;
+}
+
+fllf_status fllf_filter_host(fllf_plan p, const float* h_img, float* h_out, void* s) {
+  if (!p) return fail(FLLF_ERR_BAD_POINTER, "NULL plan");
+  if (!h_img || !h_out) return fail(FLLF_ERR_BAD_POINTER, "filter_host: NULL host pointer");
+  DeviceGuard guard(p->device);
+  const size_t bytes = (size_t)p->d.batch * p->d.H * p->d.W * sizeof(float);
+  if (!p->stage_in) {
+    if (cudaMalloc(&p->stage_in, bytes) != cudaSuccess || cudaMalloc(&p->stage_out, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(FLLF_ERR_OUT_OF_MEMORY, "staging cudaMalloc failed");
+    }
+  }
+  cudaStream_t stream = static_cast<cudaStream_t>(s);
+  cudaError_t e = cudaMemcpyAsync(p->stage_in, h_img, bytes, cudaMemcpyHostToDevice, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
+  fllf_status st = fllf_filter(p, p->stage_in, 0, p->stage_out, 0, s);
+  if (st != FLLF_OK) return st;
+  e = cudaMemcpyAsync(h_out, p->stage_out, bytes, cudaMemcpyDeviceToHost, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
+  return FLLF_OK;
+}
+
+fllf_status fllf_plan_level_dims(fllf_plan p, int level, int* H, int* W) {
+  if (!p || !H || !W) return fail(FLLF_ERR_BAD_POINTER, "NULL argument");
+  if (level < 0 || level >= p->nlev) return fail(FLLF_ERR_INVALID_ARGUMENT, "level out of range");
+  *H = p->Hs[level];
+  *W = p->Ws[level];
+  return FLLF_OK;
+}
+
+fllf_status fllf_workspace_bytes(fllf_plan p, size_t* bytes) {
+  if (!p || !bytes) return fail(FLLF_ERR_BAD_POINTER, "NULL argument");
+  *bytes = p->ws_bytes;
+  return FLLF_OK;
+}
+
+fllf_status fllf_read_pyramid(fllf_plan p, int frame, int level, int channel, float* d_dst,
+                              size_t dst_pitch_bytes, void* s) {
+  if (!p || !d_dst) return fail(FLLF_ERR_BAD_POINTER, "NULL argument");
+  if (!p->built) return fail(FLLF_ERR_NOT_BUILT, "read_pyramid before build");
+  if (level < 1 || level >= p->nlev || frame < 0 || frame >= p->d.batch || channel < 0 || channel > p->KL)
+    return fail(FLLF_ERR_INVALID_ARGUMENT, "read_pyramid: frame/level/channel out of range");
+  DeviceGuard guard(p->device);
+  const fllf::DevLevel& L = p->lv[level];
+  const void* src;
+  size_t spitch, wbytes;
+  if (channel == 0) {
+    src = L.G + (long long)frame * L.fstride_r;
+    spitch = (size_t)L.pitch * sizeof(float);
+    wbytes = (size_t)L.W * sizeof(float);
+  } else {
+    src = L.Z + (long long)frame * L.fstride_z + (long long)(channel - 1) * L.kstride_z;
+    spitch = (size_t)L.pitch * sizeof(float2);
+    wbytes = (size_t)L.W * sizeof(float2);
+  }
+  if (dst_pitch_bytes == 0) dst_pitch_bytes = wbytes;
+  if (dst_pitch_bytes < wbytes) return fail(FLLF_ERR_BAD_POINTER, "read_pyramid: destination pitch too small");
+  cudaError_t e = cudaMemcpy2DAsync(d_dst, dst_pitch_bytes, src, spitch, wbytes, (size_t)L.H,
+                                    cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(s));
+  if (e != cudaSuccess) return cuda_fail(e, "read_pyramid copy");
+  return FLLF_OK;
+}
+
+int fllf_plan_last_launch_count(fllf_plan p) { return p ? p->last_launches : 0; }
+
+fllf_status fllf_plan_set_profiling(fllf_plan p, int enable) {
+  if (!p) return fail(FLLF_ERR_BAD_POINTER, "NULL plan");
+  p->profiling = enable != 0;
+  p->nrec = 0;
+  return FLLF_OK;
+}
+
+fllf_status fllf_plan_kernel_times(fllf_plan p, int capacity, int* kind, int* level, float* ms, int* count) {
+  if (!p || !count) return fail(FLLF_ERR_BAD_POINTER, "NULL argument");
+  DeviceGuard guard(p->device);
+  const int n = std::min(capacity, p->nrec);
+  for (int i = 0; i < n; ++i) {
+    cudaError_t e = cudaEventSynchronize(p->ev_stop[i]);
+    if (e != cudaSuccess) return cuda_fail(e, "kernel_times: event sync");
+    float t = 0.f;
+    e = cudaEventElapsedTime(&t, p->ev_start[i], p->ev_stop[i]);
+    if (e != cudaSuccess) return cuda_fail(e, "kernel_times: elapsed");
+    if (kind) kind[i] = p->rec_kind[i];
+    if (level) level[i] = p->rec_level[i];
+    if (ms) ms[i] = t;
+  }
+  *count = n;
+  return FLLF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,71 @@
+// Internal structures shared by the host code (fllf_host.cpp) and the kernels
+// (fllf_kernels.cu).  Not part of the C ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fllf.h"
+
+namespace fllf {
+
+// One stored pyramid level l >= 1 (all frames).  Real planes (G, D, map
+// pyramids) have `pitch` floats per row; complex planes Z_{l,k} have `pitch`
+// float2 per row, each float2 = (S~, C~) = (Im, Re) of Z = C~ + i S~.
+struct DevLevel {
+  int H, W;
+  int pitch;           // elements per row (floats for real planes, float2 for complex)
+  float* G;            // G_l[I]
+  float* D;            // D_l = O_l - G_l (collapse from level l of the output pyramid)
+  float2* Z;           // Z_{l,k}, local orders k = 0..KL-1
+  float* MS;           // G_l[sigma_r map]   (MAPS mode, shared by frames)
+  float* MM;           // G_l[m map]
+  long long fstride_r; // floats per frame for real planes  (H*pitch)
+  long long kstride_z; // float2 per k plane                  (H*pitch)
+  long long fstride_z; // float2 per frame                    (KL*H*pitch)
+};
+
+// A caller-owned full-resolution real plane (level 0).
+struct DevImage {
+  const float* p;
+  int H, W;
+  long long pitch;     // floats per row
+  long long fstride;   // floats per frame
+};
+
+struct BuildParams {
+  DevImage img;        // build0: the image (level 0); map build at level 0: sigma map
+  DevImage img2;       // map build at level 0: m map
+  DevLevel src;        // level l (l >= 1) source
+  DevLevel dst;        // level l+1 destination
+  int Hf, Wf, Hc, Wc;  // fine (l) and coarse (l+1) dims
+  int KL;              // local number of orders
+  int kbase;           // global order of local channel 0 (k_begin, 1-based)
+  int nchunks;         // complex channel chunks per frame
+  int rows_per_strip;  // coarse rows per warp
+  int maps;            // 1: build the (sigma, m) map pyramids instead of G/Z
+  float invT;          // 1/T
+};
+
+struct ApplyParams {
+  DevImage img;        // level-0 input image I (LEVEL0 kernels)
+  float* out;          // level-0 output O (LEVEL0 kernels)
+  long long out_pitch; // floats
+  long long out_fstride;
+  DevImage smap, mmap; // MAPS at level 0: user maps (fstride 0)
+  DevLevel fine;       // level l (for l >= 1)
+  DevLevel coarse;     // level l+1
+  int Hf, Wf, Hc, Wc;
+  int KL, kbase;
+  int include_base;
+  float invT;          // 1/T
+  float c0;            // MAPS: 2 omega_1 sqrt(2 pi) / T
+  float hq;            // MAPS: omega_1^2 / 2
+  float a[FLLF_MAX_K]; // uniform a_k (SCALAR/COEFFS), local order index
+};
+
+// Kernel launchers (fllf_kernels.cu).  Return cudaGetLastError() after launch.
+cudaError_t launch_build(const BuildParams& p, int level_src, int batch, cudaStream_t s);
+cudaError_t launch_apply(const ApplyParams& p, int level_fine, bool has_d, bool maps, int batch,
+                         cudaStream_t s);
+
+}  // namespace fllf

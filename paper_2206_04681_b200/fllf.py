@@ -1,0 +1,304 @@
+"""Thin Python binding of the libfllf C ABI (include/fllf.h).
+
+Argument marshalling only: every step of the path runs in the CUDA kernels of
+libfllf.so.  Functions carry the C names; tensors are torch CUDA tensors
+(PyTorch is used for device memory and streams, nothing else).  There is no
+CPU fallback: importing this module raises if libfllf.so is missing, and the
+compute calls raise on CPU tensors or without a CUDA device.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+from dataclasses import dataclass
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libfllf.so")
+HEADER_PATH = os.path.join(os.path.dirname(_PKG), "include", "fllf.h")
+
+FLLF_OK = 0
+FLLF_ERR_INVALID_ARGUMENT = 1
+FLLF_ERR_TOO_MANY_LEVELS = 2
+FLLF_ERR_OUT_OF_MEMORY = 3
+FLLF_ERR_CUDA = 4
+FLLF_ERR_NOT_BUILT = 5
+FLLF_ERR_BAD_POINTER = 6
+FLLF_SCALAR, FLLF_COEFFS, FLLF_MAPS = 0, 1, 2
+FLLF_MAX_K = 32
+FLLF_MAX_LEVELS = 16
+
+
+class FllfError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"{status_name(status)}: {message}")
+        self.status = status
+
+
+class fllf_plan_desc(ctypes.Structure):
+    _fields_ = [("H", ctypes.c_int), ("W", ctypes.c_int), ("levels", ctypes.c_int),
+                ("K", ctypes.c_int), ("T", ctypes.c_double), ("sigma_r", ctypes.c_double),
+                ("m", ctypes.c_double), ("batch", ctypes.c_int), ("k_begin", ctypes.c_int),
+                ("k_end", ctypes.c_int), ("include_base", ctypes.c_int), ("device", ctypes.c_int)]
+
+
+class fllf_apply_args(ctypes.Structure):
+    _fields_ = [("mode", ctypes.c_int), ("a_k", ctypes.POINTER(ctypes.c_double)),
+                ("d_sigma_r", ctypes.c_void_p), ("d_m", ctypes.c_void_p),
+                ("map_pitch_bytes", ctypes.c_size_t)]
+
+
+_P = ctypes.c_void_p
+_SIGS = {
+    "fllf_plan_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                        ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                        ctypes.POINTER(_P)]),
+    "fllf_plan_create_ex": (ctypes.c_int, [ctypes.POINTER(fllf_plan_desc), ctypes.POINTER(_P)]),
+    "fllf_destroy": (ctypes.c_int, [_P]),
+    "fllf_build_fourier_pyramids": (ctypes.c_int, [_P, _P, ctypes.c_size_t, _P]),
+    "fllf_apply": (ctypes.c_int, [_P, ctypes.POINTER(fllf_apply_args), _P, ctypes.c_size_t, _P]),
+    "fllf_filter": (ctypes.c_int, [_P, _P, ctypes.c_size_t, _P, ctypes.c_size_t, _P]),
+    "fllf_filter_host": (ctypes.c_int, [_P, _P, _P, _P]),
+    "fllf_coefficients": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, ctypes.c_double,
+                                         ctypes.c_double, ctypes.POINTER(ctypes.c_double),
+                                         ctypes.POINTER(ctypes.c_double)]),
+    "fllf_plan_level_dims": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                                            ctypes.POINTER(ctypes.c_int)]),
+    "fllf_workspace_bytes": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_size_t)]),
+    "fllf_read_pyramid": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P,
+                                         ctypes.c_size_t, _P]),
+    "fllf_plan_last_launch_count": (ctypes.c_int, [_P]),
+    "fllf_plan_set_profiling": (ctypes.c_int, [_P, ctypes.c_int]),
+    "fllf_plan_kernel_times": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                                              ctypes.POINTER(ctypes.c_int),
+                                              ctypes.POINTER(ctypes.c_float),
+                                              ctypes.POINTER(ctypes.c_int)]),
+    "fllf_status_string": (ctypes.c_char_p, [ctypes.c_int]),
+    "fllf_last_error_message": (ctypes.c_char_p, []),
+}
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with "
+                          "`python -m paper_2206_04681_b200.build` (there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in _SIGS.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+def header_symbols() -> list[str]:
+    """Every function the C header declares (used by the ABI test)."""
+    txt = open(HEADER_PATH).read()
+    return sorted(set(re.findall(r"FLLF_API\s+[\w\s\*]*?\b(fllf_\w+)\s*\(", txt)))
+
+
+def status_name(st: int) -> str:
+    return lib.fllf_status_string(int(st)).decode()
+
+
+def _check(st: int) -> None:
+    if st != FLLF_OK:
+        raise FllfError(st, lib.fllf_last_error_message().decode())
+
+
+# ------------------------------------------------------------- marshalling
+def _stream_handle(stream) -> int | None:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _dev_image(t, name: str):
+    """(pointer, pitch_bytes) of a CUDA fp32 tensor [..., H, W] with unit column stride."""
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor (libfllf has no CPU fallback)")
+    if t.dtype != torch.float32 or t.stride(-1) != 1:
+        raise TypeError(f"{name} must be float32 with unit column stride")
+    if t.dim() >= 3 and t.shape[0] > 1 and t.stride(-3) != t.shape[-2] * t.stride(-2):
+        raise TypeError(f"{name}: frames must be contiguous")
+    return t.data_ptr(), t.stride(-2) * 4
+
+
+# ------------------------------------------------------------- C-ABI names
+def fllf_plan_create(H, W, levels, K, T, sigma_r, m) -> int:
+    h = _P()
+    _check(lib.fllf_plan_create(H, W, levels, K, float(T), float(sigma_r), float(m), ctypes.byref(h)))
+    return h.value
+
+
+def fllf_plan_create_ex(H, W, levels, K, T, sigma_r=30.0, m=1.0, batch=1, k_begin=0, k_end=0,
+                        include_base=True, device=-1) -> int:
+    d = fllf_plan_desc(H, W, levels, K, float(T), float(sigma_r), float(m), batch, k_begin, k_end,
+                       1 if include_base else 0, device)
+    h = _P()
+    _check(lib.fllf_plan_create_ex(ctypes.byref(d), ctypes.byref(h)))
+    return h.value
+
+
+def fllf_destroy(plan) -> None:
+    _check(lib.fllf_destroy(plan))
+
+
+def fllf_build_fourier_pyramids(plan, img, stream=None) -> None:
+    ptr, pitch = _dev_image(img, "img")
+    _check(lib.fllf_build_fourier_pyramids(plan, ptr, pitch, _stream_handle(stream)))
+
+
+def fllf_apply(plan, out, mode=FLLF_SCALAR, a_k=None, sigma_map=None, m_map=None, stream=None) -> None:
+    optr, opitch = _dev_image(out, "out")
+    args = fllf_apply_args()
+    args.mode = mode
+    keep = None
+    if mode == FLLF_COEFFS:
+        keep = np.ascontiguousarray(np.asarray(a_k, dtype=np.float64))
+        args.a_k = keep.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    elif mode == FLLF_MAPS:
+        sp, spitch = _dev_image(sigma_map, "sigma_map")
+        mp, mpitch = _dev_image(m_map, "m_map")
+        if spitch != mpitch:
+            raise ValueError("sigma and m maps must share a pitch")
+        args.d_sigma_r, args.d_m, args.map_pitch_bytes = sp, mp, spitch
+    _check(lib.fllf_apply(plan, ctypes.byref(args), optr, opitch, _stream_handle(stream)))
+    del keep
+
+
+def fllf_filter(plan, img, out, stream=None) -> None:
+    iptr, ipitch = _dev_image(img, "img")
+    optr, opitch = _dev_image(out, "out")
+    _check(lib.fllf_filter(plan, iptr, ipitch, optr, opitch, _stream_handle(stream)))
+
+
+def fllf_filter_host(plan, h_img, h_out, stream=None) -> None:
+    """h_img / h_out: contiguous float32 CPU tensors (pin them for async copies)."""
+    for t, n in ((h_img, "h_img"), (h_out, "h_out")):
+        if t.is_cuda or not t.is_contiguous():
+            raise TypeError(f"{n} must be a contiguous host tensor")
+    _check(lib.fllf_filter_host(plan, h_img.data_ptr(), h_out.data_ptr(), _stream_handle(stream)))
+
+
+def fllf_coefficients(K, T, sigma_r, m):
+    om = (ctypes.c_double * K)()
+    a = (ctypes.c_double * K)()
+    _check(lib.fllf_coefficients(K, float(T), float(sigma_r), float(m), om, a))
+    return np.array(om[:]), np.array(a[:])
+
+
+def fllf_plan_level_dims(plan, level):
+    h, w = ctypes.c_int(), ctypes.c_int()
+    _check(lib.fllf_plan_level_dims(plan, level, ctypes.byref(h), ctypes.byref(w)))
+    return h.value, w.value
+
+
+def fllf_workspace_bytes(plan) -> int:
+    b = ctypes.c_size_t()
+    _check(lib.fllf_workspace_bytes(plan, ctypes.byref(b)))
+    return b.value
+
+
+def fllf_read_pyramid(plan, frame, level, channel, dst, stream=None) -> None:
+    ptr, pitch = _dev_image(dst, "dst")
+    _check(lib.fllf_read_pyramid(plan, frame, level, channel, ptr, pitch, _stream_handle(stream)))
+
+
+def fllf_plan_last_launch_count(plan) -> int:
+    return int(lib.fllf_plan_last_launch_count(plan))
+
+
+KERNEL_KINDS = {0: "build0", 1: "build", 2: "mapbuild", 3: "apply", 4: "apply0"}
+
+
+def fllf_plan_set_profiling(plan, enable: bool) -> None:
+    _check(lib.fllf_plan_set_profiling(plan, 1 if enable else 0))
+
+
+def fllf_plan_kernel_times(plan, capacity: int = 64):
+    """[(kind name, level, milliseconds)] for the launches of the last build(+apply)."""
+    kind = (ctypes.c_int * capacity)()
+    level = (ctypes.c_int * capacity)()
+    ms = (ctypes.c_float * capacity)()
+    n = ctypes.c_int()
+    _check(lib.fllf_plan_kernel_times(plan, capacity, kind, level, ms, ctypes.byref(n)))
+    return [(KERNEL_KINDS[kind[i]], level[i], float(ms[i])) for i in range(n.value)]
+
+
+# ------------------------------------------------------------- convenience
+@dataclass
+class Plan:
+    """RAII wrapper around an fllf_plan (same arguments as fllf_plan_create_ex)."""
+    H: int
+    W: int
+    levels: int
+    K: int
+    T: float = 510.0
+    sigma_r: float = 30.0
+    m: float = 1.0
+    batch: int = 1
+    k_begin: int = 0
+    k_end: int = 0
+    include_base: bool = True
+    device: int = -1
+
+    def __post_init__(self):
+        self.handle = fllf_plan_create_ex(self.H, self.W, self.levels, self.K, self.T, self.sigma_r,
+                                          self.m, self.batch, self.k_begin, self.k_end,
+                                          self.include_base, self.device)
+
+    def build(self, img, stream=None):
+        fllf_build_fourier_pyramids(self.handle, img, stream)
+
+    def apply(self, out, **kw):
+        fllf_apply(self.handle, out, **kw)
+
+    def filter(self, img, out, stream=None):
+        fllf_filter(self.handle, img, out, stream)
+
+    def level_dims(self, level):
+        return fllf_plan_level_dims(self.handle, level)
+
+    def read_pyramid(self, frame, level, channel, dst, stream=None):
+        fllf_read_pyramid(self.handle, frame, level, channel, dst, stream)
+
+    @property
+    def launches(self) -> int:
+        return fllf_plan_last_launch_count(self.handle)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            fllf_destroy(self.handle)
+            self.handle = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def fourier_llf(img, levels, K, T=510.0, sigma_r=30.0, m=1.0, out=None):
+    """One-shot Fourier LLF of a CUDA fp32 image [H, W] or batch [B, H, W]."""
+    import torch
+    B = img.shape[0] if img.dim() == 3 else 1
+    H, W = img.shape[-2:]
+    if out is None:
+        out = torch.empty_like(img)
+    with Plan(H, W, levels, K, T, sigma_r, m, batch=B) as p:
+        p.filter(img, out)
+        torch.cuda.current_stream().synchronize()
+    return out
