@@ -131,7 +131,10 @@ FLLF_API fllf_status fllf_build_fourier_pyramids(fllf_plan p, const float* d_img
 FLLF_API fllf_status fllf_apply(fllf_plan p, const fllf_apply_args* a, float* d_out,
                        size_t out_pitch_bytes, void* s);
 
-/* build + apply(SCALAR) in one call (the common one-shot filter). */
+/* build + apply(SCALAR) in one call (the common one-shot filter).  The launch
+ * sequence is captured once into a CUDA graph (per plan, input/output buffer
+ * pair and profiling flag) and replayed on `s`; FLLF_NO_GRAPH=1 in the
+ * environment or fllf_plan_set_graphs(p, 0) launches the kernels directly. */
 FLLF_API fllf_status fllf_filter(fllf_plan p, const float* d_img, size_t in_pitch_bytes, float* d_out,
                         size_t out_pitch_bytes, void* s);
 
@@ -164,6 +167,7 @@ FLLF_API int fllf_plan_last_launch_count(fllf_plan p);
  * duration in milliseconds; *count = number of records (<= capacity). */
 enum { FLLF_K_BUILD0 = 0, FLLF_K_BUILD = 1, FLLF_K_MAPBUILD = 2, FLLF_K_APPLY = 3, FLLF_K_APPLY0 = 4 };
 FLLF_API fllf_status fllf_plan_set_profiling(fllf_plan p, int enable);
+FLLF_API fllf_status fllf_plan_set_graphs(fllf_plan p, int enable);
 FLLF_API fllf_status fllf_plan_kernel_times(fllf_plan p, int capacity, int* kind, int* level,
                                             float* ms, int* count);
 

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -74,6 +75,18 @@ struct fllf_plan_s {
   std::vector<cudaEvent_t> ev_start, ev_stop;
   std::vector<int> rec_kind, rec_level;
   int nrec = 0;
+  // CUDA graph of the whole filter sequence (build + apply), replayed on the
+  // caller's stream; re-captured when the buffers or the profiling flag change
+  bool use_graph = true;
+  bool capturing = false;
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  const void* g_in = nullptr;
+  const void* g_out = nullptr;
+  size_t g_in_pitch = 0, g_out_pitch = 0;
+  bool g_prof = false;
+  int g_launches = 0;
+  int g_nrec = 0;
 };
 
 namespace {
@@ -96,10 +109,11 @@ struct ProfScope {
     }
     p->rec_kind[idx] = kind;
     p->rec_level[idx] = level;
-    cudaEventRecord(p->ev_start[idx], s);
+    cudaEventRecordWithFlags(p->ev_start[idx], s, p->capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
   }
   ~ProfScope() {
-    if (idx >= 0) cudaEventRecord(p->ev_stop[idx], s);
+    if (idx >= 0)
+      cudaEventRecordWithFlags(p->ev_stop[idx], s, p->capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
   }
 };
 }  // namespace
@@ -179,6 +193,10 @@ fllf_status fllf_plan_create_ex(const fllf_plan_desc* din, fllf_plan* out) {
   p->KL = d.k_end - d.k_begin;
   p->kb = d.k_begin;
   p->nlev = d.levels;
+  {
+    const char* ng = std::getenv("FLLF_NO_GRAPH");
+    p->use_graph = !(ng && ng[0] == '1');
+  }
   int dev = d.device;
   if (dev < 0) {
     if (cudaGetDevice(&dev) != cudaSuccess) {
@@ -254,6 +272,8 @@ fllf_status fllf_destroy(fllf_plan p) {
     if (p->stage_out) cudaFree(p->stage_out);
     for (cudaEvent_t e : p->ev_start) cudaEventDestroy(e);
     for (cudaEvent_t e : p->ev_stop) cudaEventDestroy(e);
+    if (p->gexec) cudaGraphExecDestroy(p->gexec);
+    if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
     cudaGetLastError();
   }
   delete p;
@@ -379,6 +399,13 @@ fllf_status fllf_apply(fllf_plan p, const fllf_apply_args* a, float* d_out, size
       }
     }
   }
+  for (int i = 0; i < p->KL; ++i) {
+    const float a = ap.a[i];
+    ap.wk[i][0] = make_float2(a, a);
+    ap.wk[i][1] = make_float2(-a / 64.f, -a / 64.f);
+    ap.wk[i][2] = make_float2(-a / 16.f, -a / 16.f);
+    ap.wk[i][3] = make_float2(-a / 4.f, -a / 4.f);
+  }
   int launches = 0;
   if (p->last_was_apply) p->nrec = 0;
   p->last_was_apply = true;
@@ -444,14 +471,68 @@ fllf_status fllf_apply(fllf_plan p, const fllf_apply_args* a, float* d_out, size
   return FLLF_OK;
 }
 
-fllf_status fllf_filter(fllf_plan p, const float* d_img, size_t in_pitch_bytes, float* d_out,
-                        size_t out_pitch_bytes, void* s) {
+static fllf_status filter_eager(fllf_plan p, const float* d_img, size_t in_pitch_bytes, float* d_out,
+                                size_t out_pitch_bytes, void* s) {
   fllf_status st = fllf_build_fourier_pyramids(p, d_img, in_pitch_bytes, s);
   if (st != FLLF_OK) return st;
   const int nb = p->last_launches;
   st = fllf_apply(p, nullptr, d_out, out_pitch_bytes, s);
   if (st == FLLF_OK) p->last_launches += nb;
   return st;
+}
+
+fllf_status fllf_filter(fllf_plan p, const float* d_img, size_t in_pitch_bytes, float* d_out,
+                        size_t out_pitch_bytes, void* s) {
+  if (!p) return fail(FLLF_ERR_BAD_POINTER, "NULL plan");
+  if (!p->use_graph) return filter_eager(p, d_img, in_pitch_bytes, d_out, out_pitch_bytes, s);
+  DeviceGuard guard(p->device);
+  const bool hit = p->gexec && p->g_in == d_img && p->g_out == d_out && p->g_in_pitch == in_pitch_bytes &&
+                   p->g_out_pitch == out_pitch_bytes && p->g_prof == p->profiling;
+  if (!hit) {
+    if (p->gexec) {
+      cudaGraphExecDestroy(p->gexec);
+      p->gexec = nullptr;
+    }
+    if (!p->cap_stream) {
+      cudaError_t e = cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking);
+      if (e != cudaSuccess) return cuda_fail(e, "capture stream");
+    }
+    cudaError_t e = cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamBeginCapture");
+    p->capturing = true;
+    fllf_status st = filter_eager(p, d_img, in_pitch_bytes, d_out, out_pitch_bytes, p->cap_stream);
+    p->capturing = false;
+    cudaGraph_t graph = nullptr;
+    e = cudaStreamEndCapture(p->cap_stream, &graph);
+    if (st != FLLF_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return st;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+    e = cudaGraphInstantiate(&p->gexec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) {
+      p->gexec = nullptr;
+      return cuda_fail(e, "cudaGraphInstantiate");
+    }
+    p->g_in = d_img;
+    p->g_out = d_out;
+    p->g_in_pitch = in_pitch_bytes;
+    p->g_out_pitch = out_pitch_bytes;
+    p->g_prof = p->profiling;
+    p->g_launches = p->last_launches;
+    p->g_nrec = p->nrec;
+  }
+  cudaError_t e = cudaGraphLaunch(p->gexec, static_cast<cudaStream_t>(s));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGraphLaunch");
+  // the replay leaves the plan in the state of a fresh build + apply
+  p->built = true;
+  p->img = d_img;
+  p->img_pitch = (long long)((in_pitch_bytes ? in_pitch_bytes : (size_t)p->d.W * 4) / 4);
+  p->last_was_apply = true;
+  p->last_launches = p->g_launches;
+  p->nrec = p->g_nrec;
+  return FLLF_OK;
 }
 
 fllf_status fllf_filter_host(fllf_plan p, const float* h_img, float* h_out, void* s) {
@@ -522,6 +603,12 @@ fllf_status fllf_plan_set_profiling(fllf_plan p, int enable) {
   if (!p) return fail(FLLF_ERR_BAD_POINTER, "NULL plan");
   p->profiling = enable != 0;
   p->nrec = 0;
+  return FLLF_OK;
+}
+
+fllf_status fllf_plan_set_graphs(fllf_plan p, int enable) {
+  if (!p) return fail(FLLF_ERR_BAD_POINTER, "NULL plan");
+  p->use_graph = enable != 0;
   return FLLF_OK;
 }
 

@@ -61,6 +61,11 @@ struct ApplyParams {
   float c0;            // MAPS: 2 omega_1 sqrt(2 pi) / T
   float hq;            // MAPS: omega_1^2 / 2
   float a[FLLF_MAX_K]; // uniform a_k (SCALAR/COEFFS), local order index
+  // uniform weights per local order k as broadcast pairs for packed math:
+  // [0] = (a, a), [1] = -(a/64) (even row, even col), [2] = -(a/16) (mixed),
+  // [3] = -(a/4) (odd row, odd col): the polyphase up-sampling scales folded
+  // into a_k
+  float2 wk[FLLF_MAX_K][4];
 };
 
 // Kernel launchers (fllf_kernels.cu).  Return cudaGetLastError() after launch.

@@ -71,6 +71,7 @@ _SIGS = {
                                          ctypes.c_size_t, _P]),
     "fllf_plan_last_launch_count": (ctypes.c_int, [_P]),
     "fllf_plan_set_profiling": (ctypes.c_int, [_P, ctypes.c_int]),
+    "fllf_plan_set_graphs": (ctypes.c_int, [_P, ctypes.c_int]),
     "fllf_plan_kernel_times": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
                                               ctypes.POINTER(ctypes.c_int),
                                               ctypes.POINTER(ctypes.c_float),
@@ -220,6 +221,10 @@ KERNEL_KINDS = {0: "build0", 1: "build", 2: "mapbuild", 3: "apply", 4: "apply0"}
 
 def fllf_plan_set_profiling(plan, enable: bool) -> None:
     _check(lib.fllf_plan_set_profiling(plan, 1 if enable else 0))
+
+
+def fllf_plan_set_graphs(plan, enable: bool) -> None:
+    _check(lib.fllf_plan_set_graphs(plan, 1 if enable else 0))
 
 
 def fllf_plan_kernel_times(plan, capacity: int = 64):

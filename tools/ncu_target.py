@@ -1,0 +1,44 @@
+"""Small fixed workload for ncu captures: N filter calls of one BASELINE config.
+
+    python tools/ncu_target.py [--workload config2|config5|config3|config4] [--iters 2]
+"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2206_04681_b200 import fllf as F  # noqa: E402
+from paper_2206_04681_b200 import synth  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="config2")
+    ap.add_argument("--iters", type=int, default=2)
+    a = ap.parse_args()
+    cfg = int(a.workload[-1])
+    c = synth.CONFIGS[cfg]
+    if cfg == 5:
+        x = synth.config5_frames(16)
+    elif cfg in (3, 4):
+        x = synth.config2_image(seed=4000, H=c["H"], W=c["W"])[None]
+    else:
+        x = synth.config2_image()[None] if cfg == 2 else synth.config1_image()[None]
+    d_in = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    d_out = torch.empty_like(d_in)
+    sig = c.get("sigma_r", 30.0)
+    m = c.get("m", 2.0)
+    with F.Plan(c["H"], c["W"], c["levels"], c["K"], c["T"], sig, m, batch=d_in.shape[0]) as p:
+        for _ in range(a.iters):
+            p.filter(d_in, d_out)
+        torch.cuda.synchronize()
+        print("launches per filter:", p.launches, "out mean", float(d_out.mean()))
+
+
+if __name__ == "__main__":
+    main()
