@@ -224,16 +224,15 @@ fllf_status fllf_plan_create_ex(const fllf_plan_desc* din, fllf_plan* out) {
   size_t off = 0;
   std::vector<size_t> offG(d.levels), offD(d.levels), offZ(d.levels);
   for (int l = 1; l < d.levels; ++l) {
-    const size_t pitch_r = align_up((size_t)p->Ws[l], 32);  // floats (128 B)
-    const size_t pitch_c = align_up((size_t)p->Ws[l], 16);  // float2 (128 B)
-    // one pitch value serves both kinds: use the float2 pitch rounded to 32
-    const size_t pitch = std::max(pitch_r, align_up(pitch_c, 32));
+    const size_t pitch = align_up((size_t)p->Ws[l], 32);                              // floats (128 B)
+    const size_t zpitch = align_up((size_t)p->Ws[l] + fllf::ZHALO + fllf::ZPAD, 16);  // float2 (128 B)
     fllf::DevLevel& L = p->lv[l];
     L.H = p->Hs[l];
     L.W = p->Ws[l];
     L.pitch = (int)pitch;
+    L.zpitch = (int)zpitch;
     L.fstride_r = (long long)(L.H * pitch);
-    L.kstride_z = (long long)(L.H * pitch);
+    L.kstride_z = (long long)(L.H * zpitch);
     L.fstride_z = (long long)p->KL * L.kstride_z;
     offG[l] = off;
     off = align_up(off + B * L.fstride_r * sizeof(float), 256);
@@ -255,7 +254,14 @@ fllf_status fllf_plan_create_ex(const fllf_plan_desc* din, fllf_plan* out) {
   for (int l = 1; l < d.levels; ++l) {
     p->lv[l].G = reinterpret_cast<float*>(base + offG[l]);
     p->lv[l].D = reinterpret_cast<float*>(base + offD[l]);
-    p->lv[l].Z = reinterpret_cast<float2*>(base + offZ[l]);
+    p->lv[l].Z = reinterpret_cast<float2*>(base + offZ[l]) + fllf::ZHALO;
+  }
+  // halo / padding cells that no kernel writes must hold finite values
+  e = cudaMemset(p->ws, 0, off);
+  if (e != cudaSuccess) {
+    cudaFree(p->ws);
+    delete p;
+    return cuda_fail(e, "workspace memset");
   }
   *out = p;
   return FLLF_OK;
@@ -586,7 +592,7 @@ fllf_status fllf_read_pyramid(fllf_plan p, int frame, int level, int channel, fl
     wbytes = (size_t)L.W * sizeof(float);
   } else {
     src = L.Z + (long long)frame * L.fstride_z + (long long)(channel - 1) * L.kstride_z;
-    spitch = (size_t)L.pitch * sizeof(float2);
+    spitch = (size_t)L.zpitch * sizeof(float2);
     wbytes = (size_t)L.W * sizeof(float2);
   }
   if (dst_pitch_bytes == 0) dst_pitch_bytes = wbytes;

@@ -8,20 +8,30 @@
 
 namespace fllf {
 
+// Z planes carry ZHALO float2 columns left of column 0 and ZPAD columns of
+// padding right of column W-1.  Column -1 holds x_1 and column W holds
+// x_{W-1} or x_{W-2} (the up-sampling border rule for the finer level's width
+// parity), written by the producing k_build; the apply kernel then stages
+// whole, 16-byte-aligned row segments with TMA bulk copies and never maps a
+// column index.
+constexpr int ZHALO = 4;
+constexpr int ZPAD = 128;
+
 // One stored pyramid level l >= 1 (all frames).  Real planes (G, D, map
-// pyramids) have `pitch` floats per row; complex planes Z_{l,k} have `pitch`
+// pyramids) have `pitch` floats per row; complex planes Z_{l,k} have `zpitch`
 // float2 per row, each float2 = (S~, C~) = (Im, Re) of Z = C~ + i S~.
 struct DevLevel {
   int H, W;
-  int pitch;           // elements per row (floats for real planes, float2 for complex)
+  int pitch;           // floats per row of the real planes
+  int zpitch;          // float2 per row of the complex planes (incl. halo + pad)
   float* G;            // G_l[I]
   float* D;            // D_l = O_l - G_l (collapse from level l of the output pyramid)
-  float2* Z;           // Z_{l,k}, local orders k = 0..KL-1
+  float2* Z;           // Z_{l,k} column 0 of row 0, local orders k = 0..KL-1
   float* MS;           // G_l[sigma_r map]   (MAPS mode, shared by frames)
   float* MM;           // G_l[m map]
   long long fstride_r; // floats per frame for real planes  (H*pitch)
-  long long kstride_z; // float2 per k plane                  (H*pitch)
-  long long fstride_z; // float2 per frame                    (KL*H*pitch)
+  long long kstride_z; // float2 per k plane                  (H*zpitch)
+  long long fstride_z; // float2 per frame                    (KL*H*zpitch)
 };
 
 // A caller-owned full-resolution real plane (level 0).

@@ -26,17 +26,21 @@
 //              (the same-level level-0 term vanishes).  All K orders
 //              are accumulated in registers; e^{i w_k g} comes from one
 //              sincos(w_1 g) and a Chebyshev recurrence.
-//              Layout: thread owns a 2x4 block of fine pixels (one coarse row,
-//              two coarse columns); per order it reads the three coarse rows
-//              it needs (next order prefetched), coarse neighbours come from
-//              warp shuffles.  Small levels split the K orders over the 4
-//              warps of a CTA (KSPLIT) and reduce through shared memory.
+//              Layout: CTA = 4 warps = 4 coarse rows x 30 coarse column
+//              pairs; thread owns a 2x4 block of fine pixels.  Per order k the
+//              CTA's 6 coarse rows (and 8 fine rows for l >= 1) of Z are staged
+//              into shared memory by TMA bulk copies (cp.async.bulk + mbarrier,
+//              4-stage ring, issued by one thread) -- the Z planes carry halo
+//              columns so every copy is a whole aligned row segment; threads
+//              read their values with LDS.128 and coarse neighbours come from
+//              warp shuffles.
 //
 // No tensor cores: this is a stencil + elementwise path (no contraction).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include "fllf_internal.h"
+#include "fllf_ptx.h"
 
 namespace fllf {
 namespace {
@@ -143,161 +147,174 @@ __device__ __forceinline__ float hfilt_r(float a, float b) {
 }
 
 // ----------------------------------------------------------------- build
-// NC complex channels per chunk, NR real channels (1: G; 2: sigma/m maps).
-template <int NC, int NR, bool FROM_IMAGE>
-__global__ void __launch_bounds__(128) k_build(const BuildParams P) {
-  constexpr int NCX = NC > 0 ? NC : 1;
-  constexpr int NCL = FROM_IMAGE ? 1 : NCX;  // complex values loaded per row
-  const int lane = threadIdx.x & 31;
-  const int cb = blockIdx.x * 4 + (threadIdx.x >> 5);
-  if (cb * 30 >= P.Wc) return;
-  const int o0 = blockIdx.y * P.rows_per_strip;
-  if (o0 >= P.Hc) return;
-  const int R = min(P.rows_per_strip, P.Hc - o0);  // output rows of this strip
-  const int chunk = blockIdx.z % P.nchunks;
-  const int frame = blockIdx.z / P.nchunks;
-  const int x = cb * 30 + lane - 1;
-  const bool store_lane = lane >= 1 && lane <= 30 && x < P.Wc;
-  const int c0 = 2 * x;
-  const bool inside = (c0 >= 0) && (c0 + 1 < P.Wf);
-  const int rc0 = refl101(c0, P.Wf), rc1 = refl101(c0 + 1, P.Wf);
-  const int k0 = chunk * NC;
-  const int nc = NC > 0 ? min(NC, P.KL - k0) : 0;
-  const bool do_real = (chunk == 0);
-
-  // ---- real planes: sources / destinations
-  const float* rsrc[NR];
-  float* rdst[NR];
-  long long rpitch;
-  bool raligned;
-  if (FROM_IMAGE) {
-    rsrc[0] = P.img.p + frame * P.img.fstride;
-    if (NR > 1) rsrc[NR - 1] = P.img2.p + frame * P.img2.fstride;
-    rpitch = P.img.pitch;
-    raligned = ((reinterpret_cast<uintptr_t>(P.img.p) & 7) == 0) && ((P.img.pitch & 1) == 0) &&
-               (NR < 2 || (((reinterpret_cast<uintptr_t>(P.img2.p) & 7) == 0) && P.img2.pitch == P.img.pitch));
-  } else {
-    if (P.maps) {
-      rsrc[0] = P.src.MS;
-      if (NR > 1) rsrc[NR - 1] = P.src.MM;
-    } else {
-      rsrc[0] = P.src.G + frame * P.src.fstride_r;
-    }
-    rpitch = P.src.pitch;
-    raligned = true;
-  }
-  if (P.maps) {
-    rdst[0] = P.dst.MS;
-    if (NR > 1) rdst[NR - 1] = P.dst.MM;
-  } else {
-    rdst[0] = P.dst.G + frame * P.dst.fstride_r;
-  }
-  const bool rvec = inside && raligned;
-
-  const float2* zsrc = nullptr;
-  float2* zdst = nullptr;
-  if (NC > 0) {
-    if (!FROM_IMAGE) zsrc = P.src.Z + frame * P.src.fstride_z + (long long)k0 * P.src.kstride_z;
-    zdst = P.dst.Z + frame * P.dst.fstride_z + (long long)k0 * P.dst.kstride_z;
-  }
-  const int g0 = P.kbase + k0;  // global order of this chunk's first channel
+// One warp = 30 coarse output columns x a strip of R output rows, for NC
+// complex channels (orders kbase + k0 .. + NC-1, exactly NC: the launcher
+// picks NC dividing the local order count) and NR real channels (1: G_l[I];
+// 2: the sigma / m maps).  EDGE = false: all 64 fine columns of the warp lie
+// inside the row, no index mapping; EDGE = true: reflect-101 per column.
+template <int NC, int NR, bool FROM_IMAGE, bool EDGE>
+struct BuildWarp {
+  static constexpr int NCX = NC > 0 ? NC : 1;
+  static constexpr int NCL = FROM_IMAGE ? 1 : NCX;  // complex values loaded per row
 
   struct Row {
     float2 r[NR];
-    float4 c[NCL];
+    float2 c[NCL][2];
   };
   struct Pair {
     Row e, o;
   };
-  auto load_row = [&](int row, Row& d) {
+
+  const BuildParams& P;
+  int o0, x, c0, rc0, rc1, g0;
+  bool store_lane, halo_l, halo_r, do_real;
+  const float* rsrc[NR];
+  float* rdst[NR];
+  long long rpitch;
+  const float2* zsrc;
+  float2* zdst;
+  // two role-swapping accumulators per channel and column half (see vstep)
+  float2 S0c[NCX][2], S1c[NCX][2];
+  float2 S0r[NR], S1r[NR];
+
+  __device__ __forceinline__ BuildWarp(const BuildParams& P_, int cb, int o0_, int chunk, int frame) : P(P_), o0(o0_) {
+    const int lane = threadIdx.x & 31;
+    x = cb * 30 + lane - 1;
+    store_lane = lane >= 1 && lane <= 30 && x < P.Wc;
+    c0 = 2 * x;
+    rc0 = EDGE ? refl101(c0, P.Wf) : c0;
+    rc1 = EDGE ? refl101(c0 + 1, P.Wf) : c0 + 1;
+    const int k0 = chunk * NC;
+    g0 = P.kbase + k0;  // global order of this chunk's first channel
+    do_real = (chunk == 0);
+    // halo columns of the destination Z planes (see ZHALO): col -1 := x_1,
+    // col Wc := x_{Wc-1} (Wf even) or x_{Wc-2} (Wf odd)
+    halo_l = store_lane && x == 1;
+    halo_r = store_lane && x == ((P.Wf & 1) ? P.Wc - 2 : P.Wc - 1);
+    if (FROM_IMAGE) {
+      rsrc[0] = P.img.p + frame * P.img.fstride;
+      if (NR > 1) rsrc[NR - 1] = P.img2.p + frame * P.img2.fstride;
+      rpitch = P.img.pitch;
+    } else {
+      if (P.maps) {
+        rsrc[0] = P.src.MS;
+        if (NR > 1) rsrc[NR - 1] = P.src.MM;
+      } else {
+        rsrc[0] = P.src.G + frame * P.src.fstride_r;
+      }
+      rpitch = P.src.pitch;
+    }
+    if (P.maps) {
+      rdst[0] = P.dst.MS;
+      if (NR > 1) rdst[NR - 1] = P.dst.MM;
+    } else {
+      rdst[0] = P.dst.G + frame * P.dst.fstride_r;
+    }
+    zsrc = nullptr;
+    zdst = nullptr;
+    if (NC > 0) {
+      if (!FROM_IMAGE) zsrc = P.src.Z + frame * P.src.fstride_z + (long long)k0 * P.src.kstride_z;
+      zdst = P.dst.Z + frame * P.dst.fstride_z + (long long)k0 * P.dst.kstride_z;
+    }
+#pragma unroll
+    for (int i = 0; i < NCX; ++i) S0c[i][0] = S0c[i][1] = S1c[i][0] = S1c[i][1] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < NR; ++i) S0r[i] = S1r[i] = make_float2(0.f, 0.f);
+  }
+
+  __device__ __forceinline__ void load_row(int row, Row& d) const {
     const int rr = refl101(row, P.Hf);
 #pragma unroll
     for (int i = 0; i < NR; ++i) {
       const float* rp = rsrc[i] + (long long)rr * rpitch;
-      d.r[i] = rvec ? ldg2(rp + c0) : make_float2(__ldg(rp + rc0), __ldg(rp + rc1));
+      d.r[i] = EDGE ? make_float2(__ldg(rp + rc0), __ldg(rp + rc1)) : ldg2(rp + c0);
     }
     if (!FROM_IMAGE && NC > 0) {
+      const float2* zp = zsrc + (long long)rr * P.src.zpitch;
 #pragma unroll
       for (int i = 0; i < NCX; ++i) {
-        if (i < nc) {
-          const float2* zp = zsrc + (long long)i * P.src.kstride_z + (long long)rr * P.src.pitch;
-          if (inside) {
-            d.c[i] = ldg4(zp + c0);
-          } else {
-            d.c[i] = cat4(__ldg(zp + rc0), __ldg(zp + rc1));
-          }
+        const float2* q = zp + (long long)i * P.src.kstride_z;
+        if (EDGE) {
+          d.c[i][0] = __ldg(q + rc0);
+          d.c[i][1] = __ldg(q + rc1);
+        } else {
+          const float4 v = ldg4(q + c0);
+          d.c[i][0] = lo2(v);
+          d.c[i][1] = hi2(v);
         }
       }
     }
-  };
+  }
   // pair p holds rows 2(o0+p-1), 2(o0+p-1)+1 (p = 0: the two halo rows above)
-  auto load_pair = [&](int p, Pair& d) {
+  __device__ __forceinline__ void load_pair(int p, Pair& d) const {
     const int r0 = 2 * (o0 + p - 1);
     load_row(r0, d.e);
     load_row(r0 + 1, d.o);
-  };
+  }
 
-  // two role-swapping accumulators per channel (see vstep)
-  float4 S0c[NCX] = {}, S1c[NCX] = {};
-  float2 S0r[NR] = {}, S1r[NR] = {};
+  // One channel over a row pair with roles (Pc, Ac).
+  template <bool EMIT, bool ONLY>
+  __device__ __forceinline__ void chan(float2 (&Pc)[2], float2 (&Ac)[2], float2 ea_, float2 eb_, float2 oa,
+                                       float2 ob, float2* q) {
+    if (EMIT) {
+      const float2 ea = pfma(bc(W2), ea_, Pc[0]);
+      const float2 eb = pfma(bc(W2), eb_, Pc[1]);
+      const float2 h = hfilt_c(ea, eb);
+      if (store_lane) q[x] = h;
+      if (halo_l) q[-1] = h;
+      if (halo_r) q[P.Wc] = h;
+    }
+    if (!ONLY) {
+      vstep(Pc[0], Ac[0], ea_, oa);
+      vstep(Pc[1], Ac[1], eb_, ob);
+    }
+  }
 
-  // Process one row pair with roles (Pc/Pr = pending output, Ac/Ar = current).
-  // emit >= 0: finish output row `emit` with the even row and store it.
-  // only_emit: the final row (no accumulator update).
-  auto proc = [&](const Pair& d, float4 (&Pc)[NCX], float4 (&Ac)[NCX], float2 (&Pr)[NR],
-                  float2 (&Ar)[NR], int emit, bool only_emit) {
+  // One row pair with roles (Pc/Pr pending output, Ac/Ar current output).
+  // EMIT: finish output row `emit` with the even row and store it; ONLY: the
+  // final row (no accumulator update).
+  template <bool EMIT, bool ONLY>
+  __device__ __forceinline__ void proc(const Pair& d, float2 (&Pc)[NCX][2], float2 (&Ac)[NCX][2],
+                                       float2 (&Pr)[NR], float2 (&Ar)[NR], int emit) {
     if (do_real) {
 #pragma unroll
       for (int i = 0; i < NR; ++i) {
-        if (emit >= 0) {
+        if (EMIT) {
           const float2 e = pfma(bc(W2), d.e.r[i], Pr[i]);
           const float h = hfilt_r(e.x, e.y);
           if (store_lane) rdst[i][(long long)emit * P.dst.pitch + x] = h;
         }
-        if (!only_emit) vstep(Pr[i], Ar[i], d.e.r[i], d.o.r[i]);
+        if (!ONLY) vstep(Pr[i], Ar[i], d.e.r[i], d.o.r[i]);
       }
     }
     if (NC == 0) return;
-    auto chan = [&](int i, float4 ve, float4 vo) {
-      if (emit >= 0) {
-        const float2 ea = pfma(bc(W2), lo2(ve), lo2(Pc[i]));
-        const float2 eb = pfma(bc(W2), hi2(ve), hi2(Pc[i]));
-        const float2 h = hfilt_c(ea, eb);
-        if (store_lane) zdst[(long long)i * P.dst.kstride_z + (long long)emit * P.dst.pitch + x] = h;
-      }
-      if (!only_emit) {
-        float2 pa = lo2(Pc[i]), pb = hi2(Pc[i]), aa = lo2(Ac[i]), ab = hi2(Ac[i]);
-        vstep(pa, aa, lo2(ve), lo2(vo));
-        vstep(pb, ab, hi2(ve), hi2(vo));
-        Pc[i] = cat4(pa, pb);
-        Ac[i] = cat4(aa, ab);
-      }
-    };
+    float2* zrow = zdst + (long long)emit * P.dst.zpitch;
     if (FROM_IMAGE) {
       // e^{i k w_1 I} for the 4 pixels (even/odd row x col a/b), (s, c) layout
-      float2 z1[4], zc[4], zp[4], tc[4];
+      float2 zc[4], zp[4];
+      float tc[4];
       const float I4[4] = {d.e.r[0].x, d.e.r[0].y, d.o.r[0].x, d.o.r[0].y};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        float s, c;
-        sincos_turns(I4[q], P.invT, &s, &c);
-        z1[q] = make_float2(s, c);
-        tc[q] = bc(2.f * c);
+        float sn, cs;
+        sincos_turns(I4[q], P.invT, &sn, &cs);
+        const float2 z1 = make_float2(sn, cs);
+        tc[q] = 2.f * cs;
         if (g0 == 1) {
           zp[q] = make_float2(0.f, 1.f);
-          zc[q] = z1[q];
+          zc[q] = z1;
         } else {
-          zp[q] = cpow_sc(z1[q], g0 - 1);
-          zc[q] = cmul_sc(zp[q], z1[q]);
+          zp[q] = cpow_sc(z1, g0 - 1);
+          zc[q] = cmul_sc(zp[q], z1);
         }
       }
 #pragma unroll
       for (int i = 0; i < NCX; ++i) {
-        if (i < nc) {
-          chan(i, cat4(zc[0], zc[1]), cat4(zc[2], zc[3]));
+        chan<EMIT, ONLY>(Pc[i], Ac[i], zc[0], zc[1], zc[2], zc[3], zrow + (long long)i * P.dst.kstride_z);
+        if (i + 1 < NCX) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const float2 zn = pfma(tc[q], zc[q], pneg(zp[q]));
+            const float2 zn = pfma(bc(-1.f), zp[q], pmul(bc(tc[q]), zc[q]));
             zp[q] = zc[q];
             zc[q] = zn;
           }
@@ -306,81 +323,153 @@ __global__ void __launch_bounds__(128) k_build(const BuildParams P) {
     } else {
 #pragma unroll
       for (int i = 0; i < NCX; ++i)
-        if (i < nc) chan(i, d.e.c[i], d.o.c[i]);
+        chan<EMIT, ONLY>(Pc[i], Ac[i], d.e.c[i][0], d.e.c[i][1], d.o.c[i][0], d.o.c[i][1],
+                         zrow + (long long)i * P.dst.kstride_z);
     }
-  };
-
-  Pair BA, BB;
-  load_pair(0, BA);
-  load_pair(1, BB);
-  proc(BA, S1c, S0c, S1r, S0r, -1, false);  // p = 0: halo rows
-  load_pair(2, BA);
-  proc(BB, S0c, S1c, S0r, S1r, -1, false);  // p = 1: first pair, nothing to emit
-  load_pair(3, BB);
-  int p = 2;
-#pragma unroll 1
-  for (; p + 1 <= R; p += 2) {
-    proc(BA, S1c, S0c, S1r, S0r, o0 + p - 2, false);
-    load_pair(p + 2, BA);
-    proc(BB, S0c, S1c, S0r, S1r, o0 + p - 1, false);
-    load_pair(p + 3, BB);
   }
-  if (p <= R) {
-    proc(BA, S1c, S0c, S1r, S0r, o0 + p - 2, false);
-    proc(BB, S0c, S1c, S0r, S1r, o0 + R - 1, true);  // final row = even row of pair R+1
+
+  __device__ __forceinline__ void run(int R) {
+    Pair BA, BB;
+    load_pair(0, BA);
+    load_pair(1, BB);
+    proc<false, false>(BA, S1c, S0c, S1r, S0r, 0);  // p = 0: halo rows
+    load_pair(2, BA);
+    proc<false, false>(BB, S0c, S1c, S0r, S1r, 0);  // p = 1: first pair, nothing to emit
+    load_pair(3, BB);
+    int p = 2;
+#pragma unroll 1
+    for (; p + 1 <= R; p += 2) {
+      proc<true, false>(BA, S1c, S0c, S1r, S0r, o0 + p - 2);
+      load_pair(p + 2, BA);
+      proc<true, false>(BB, S0c, S1c, S0r, S1r, o0 + p - 1);
+      load_pair(p + 3, BB);
+    }
+    if (p <= R) {
+      proc<true, false>(BA, S1c, S0c, S1r, S0r, o0 + p - 2);
+      proc<true, true>(BB, S0c, S1c, S0r, S1r, o0 + R - 1);  // final row = even row of pair R+1
+    } else {
+      proc<true, true>(BA, S1c, S0c, S1r, S0r, o0 + R - 1);
+    }
+  }
+};
+
+template <int NC, int NR, bool FROM_IMAGE>
+__global__ void __launch_bounds__(32) k_build(const BuildParams P) {
+  const int cb = blockIdx.x;  // one warp per CTA: all control flow is blockIdx-uniform
+  if (cb * 30 >= P.Wc) return;
+  const int o0 = blockIdx.y * P.rows_per_strip;
+  if (o0 >= P.Hc) return;
+  const int R = min(P.rows_per_strip, P.Hc - o0);
+  const int chunk = blockIdx.z % P.nchunks;
+  const int frame = blockIdx.z / P.nchunks;
+  // are all 64 fine columns of this warp inside the row (and, for the
+  // caller's image, 8-byte aligned)?
+  bool interior = (60 * cb - 2 >= 0) && (60 * cb + 61 < P.Wf);
+  if (FROM_IMAGE)
+    interior = interior && ((reinterpret_cast<uintptr_t>(P.img.p) & 7) == 0) && ((P.img.pitch & 1) == 0) &&
+               (NR < 2 || (((reinterpret_cast<uintptr_t>(P.img2.p) & 7) == 0) && P.img2.pitch == P.img.pitch));
+  if (interior) {
+    BuildWarp<NC, NR, FROM_IMAGE, false> w(P, cb, o0, chunk, frame);
+    w.run(R);
   } else {
-    proc(BA, S1c, S0c, S1r, S0r, o0 + R - 1, true);
+    BuildWarp<NC, NR, FROM_IMAGE, true> w(P, cb, o0, chunk, frame);
+    w.run(R);
   }
 }
 
 // ----------------------------------------------------------------- apply
-template <bool LEVEL0, bool HAS_D, bool MAPS, int KSPLIT>
-__global__ void __launch_bounds__(128) k_apply(const ApplyParams P) {
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int jb = KSPLIT == 1 ? blockIdx.x * 4 + warp : blockIdx.x;
-  if (jb * 60 >= P.Wc) return;       // warp- (KSPLIT=1) or block-uniform (KSPLIT>1)
-  const int j = jb * 30 + lane - 1;  // coarse columns 2j, 2j+1 -> fine columns 4j..4j+3
-  const int r = blockIdx.y;          // coarse row -> fine rows 2r, 2r+1
+constexpr int APPLY_STAGES = 4;
+constexpr int CROW_BYTES = 64 * 8;   // 32 lanes x 2 coarse complex values
+constexpr int FROW_BYTES = 128 * 8;  // 32 lanes x 4 fine complex values
+
+template <bool LEVEL0>
+__host__ __device__ constexpr int apply_stage_bytes() {
+  return 6 * CROW_BYTES + (LEVEL0 ? 0 : 8 * FROW_BYTES);
+}
+
+template <bool LEVEL0, bool HAS_D, bool MAPS>
+__global__ void __launch_bounds__(128, 3) k_apply(const ApplyParams P) {
+  constexpr int S = APPLY_STAGES;
+  constexpr int STAGE = apply_stage_bytes<LEVEL0>();
+  constexpr int FOFF = 6 * CROW_BYTES;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t full[S];
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int jb = blockIdx.x;         // fine columns [120 jb, 120 jb + 120)
+  const int r0 = blockIdx.y * 4;     // coarse rows r0 .. r0+3, one per warp
   const int frame = blockIdx.z;
-  const bool act = lane >= 1 && lane <= 30 && 4 * j < P.Wf;
+  const int r = r0 + warp;
+  const int j = jb * 30 + lane - 1;  // coarse columns 2j, 2j+1 -> fine columns 4j..4j+3
+  const bool rowok = r < P.Hc;
+  const bool act = rowok && lane >= 1 && lane <= 30 && 4 * j < P.Wf;
+  const int KL = P.KL;
+
+  // ---- TMA producer (thread 0): per order k, 6 coarse row segments of
+  // Z_{l+1,k} (coarse cols 2j0 .. 2j0+63, j0 = 30 jb - 1) and, for l >= 1,
+  // 8 fine row segments of Z_{l,k} (fine cols 4j0 .. 4j0+127)
+  const float2* zc0 = P.coarse.Z + frame * P.coarse.fstride_z + (60 * jb - 2);
+  const float2* zf0 = LEVEL0 ? nullptr : P.fine.Z + frame * P.fine.fstride_z + (120 * jb - 4);
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](int k) {
+    const int s = k % S;
+    unsigned char* st = smem + s * STAGE;
+    mbar_arrive_expect_tx(&full[s], STAGE);
+    const float2* zc = zc0 + (long long)k * P.coarse.kstride_z;
+#pragma unroll
+    for (int t = 0; t < 6; ++t) {
+      const int cr = upmap(r0 - 1 + t, P.Hc, P.Hf);
+      tma_load_1d(st + t * CROW_BYTES, zc + (long long)cr * P.coarse.zpitch, CROW_BYTES, &full[s]);
+    }
+    if (!LEVEL0) {
+      const float2* zf = zf0 + (long long)k * P.fine.kstride_z;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int fr = min(2 * r0 + t, P.Hf - 1);
+        tma_load_1d(st + FOFF + t * FROW_BYTES, zf + (long long)fr * P.fine.zpitch, FROW_BYTES, &full[s]);
+      }
+    }
+  };
+  if (tid == 0) {
+    const int npre = KL < S ? KL : S;
+    for (int k = 0; k < npre; ++k) issue(k);
+  }
+
+  // ---- per-thread setup (overlaps the first copies)
   const bool row1 = 2 * r + 1 < P.Hf;
-  const int yf[2] = {2 * r, row1 ? 2 * r + 1 : 2 * r};
+  const int yf[2] = {min(2 * r, P.Hf - 1), min(row1 ? 2 * r + 1 : 2 * r, P.Hf - 1)};
   const int xf0 = 4 * j;
   const bool fvec_ok = xf0 >= 0 && xf0 + 3 < P.Wf;
   int xf[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) xf[q] = min(max(xf0 + q, 0), P.Wf - 1);
-
-  // coarse rows r-1, r, r+1 and columns 2j, 2j+1 (polyphase border rule)
-  const int cr[3] = {upmap(r - 1, P.Hc, P.Hf), r, upmap(r + 1, P.Hc, P.Hf)};
+  const int cr[3] = {upmap(r - 1, P.Hc, P.Hf), min(r, P.Hc - 1), upmap(r + 1, P.Hc, P.Hf)};
   const bool cvec = (2 * j >= 0) && (2 * j + 1 < P.Wc);
   const int cc0 = upmap(2 * j, P.Wc, P.Wf), cc1 = upmap(2 * j + 1, P.Wc, P.Wf);
 
-  int k_lo = 0, k_hi = P.KL;
-  if (KSPLIT > 1) {
-    const int per = (P.KL + KSPLIT - 1) / KSPLIT;
-    k_lo = min(warp * per, P.KL);
-    k_hi = min(k_lo + per, P.KL);
-  }
-
-  // ---- up(D_{l+1}) coarse rows: issue early (used after the order loop)
   float dq[3][2];
-  if (HAS_D && (KSPLIT == 1 || warp == 0)) {
+  if (HAS_D) {
     const float* dc = P.coarse.D + frame * P.coarse.fstride_r;
 #pragma unroll
     for (int t = 0; t < 3; ++t) {
       const float* rp = dc + (long long)cr[t] * P.coarse.pitch;
       if (cvec) {
         const float2 q = ldg2(rp + 2 * j);
-        dq[t][0] = q.x; dq[t][1] = q.y;
+        dq[t][0] = q.x;
+        dq[t][1] = q.y;
       } else {
-        dq[t][0] = __ldg(rp + cc0); dq[t][1] = __ldg(rp + cc1);
+        dq[t][0] = __ldg(rp + cc0);
+        dq[t][1] = __ldg(rp + cc1);
       }
     }
   }
-
-  // ---- per fine pixel p = 4*t + q (t: fine row 2r+t, q: fine col 4j+q): g
   float g[8];
   {
     const float* base;
@@ -407,28 +496,6 @@ __global__ void __launch_bounds__(128) k_apply(const ApplyParams P) {
       }
     }
   }
-
-  // Chebyshev state per pixel, (c, s) layout: z = e^{i k w_1 g}, zp = e^{i (k-1) w_1 g}
-  float2 z[8], zp[8], tc[8], acc[8];
-  const int g0 = P.kbase + k_lo;
-#pragma unroll
-  for (int p = 0; p < 8; ++p) {
-    float s, c;
-    sincos_turns(g[p], P.invT, &s, &c);
-    const float2 z1 = make_float2(c, s);
-    tc[p] = bc(2.f * c);
-    if (g0 == 1) {
-      zp[p] = make_float2(1.f, 0.f);
-      z[p] = z1;
-    } else {
-      zp[p] = cpow_cs(z1, g0 - 1);
-      z[p] = cmul_cs(zp[p], z1);
-    }
-    acc[p] = make_float2(0.f, 0.f);
-  }
-
-  // MAPS: a_k(p) = m sigma^3 c0 k exp(-k^2 hq sigma^2) (Sec. III-B; Eq. 9-11),
-  // carried as mA = a_k, mR = exp(-(2k+1) beta), mQ = exp(-2 beta)
   float mA[8], mR[8], mQ[8];
   if (MAPS) {
     const float* sptr;
@@ -447,55 +514,60 @@ __global__ void __launch_bounds__(128) k_apply(const ApplyParams P) {
         const float sg = __ldg(sptr + off), m = __ldg(mptr + off);
         const float beta = P.hq * sg * sg;
         const int p = 4 * t + q;
-        mA[p] = m * sg * sg * sg * P.c0 * (float)g0 * __expf(-(float)g0 * (float)g0 * beta);
-        mR[p] = __expf(-(float)(2 * g0 + 1) * beta);
+        const float kb = (float)P.kbase;
+        // a_k = m sigma^3 c0 k exp(-k^2 beta), carried with R = exp(-(2k+1) beta), Q = exp(-2 beta)
+        mA[p] = m * sg * sg * sg * P.c0 * kb * __expf(-kb * kb * beta);
+        mR[p] = __expf(-(2.f * kb + 1.f) * beta);
         mQ[p] = __expf(-2.f * beta);
       }
     }
   }
-
-  const float2* zc_base = P.coarse.Z + frame * P.coarse.fstride_z;
-  const float2* zf_base = LEVEL0 ? nullptr : P.fine.Z + frame * P.fine.fstride_z;
-
-  struct KData {
-    float4 q[3];  // coarse rows r-1, r, r+1 at coarse cols (2j, 2j+1)
-    float4 f[4];  // fine Z_{l,k}: rows 2r, 2r+1 x cols (4j, 4j+1), (4j+2, 4j+3)
-  };
-  auto loadk = [&](int k, KData& d) {
-    const float2* zc = zc_base + (long long)k * P.coarse.kstride_z;
+  // Chebyshev state per pixel, (c, s) layout: z = e^{i k w_1 g}, zp = e^{i (k-1) w_1 g}
+  float2 z[8], zp[8], acc[8];
+  float tc[8];
+  const int g0 = P.kbase;
 #pragma unroll
-    for (int t = 0; t < 3; ++t) {
-      const float2* rp = zc + (long long)cr[t] * P.coarse.pitch;
-      d.q[t] = cvec ? ldg4(rp + 2 * j) : cat4(__ldg(rp + cc0), __ldg(rp + cc1));
+  for (int p = 0; p < 8; ++p) {
+    float sn, cs;
+    sincos_turns(g[p], P.invT, &sn, &cs);
+    const float2 z1 = make_float2(cs, sn);
+    tc[p] = 2.f * cs;
+    if (g0 == 1) {
+      zp[p] = make_float2(1.f, 0.f);
+      z[p] = z1;
+    } else {
+      zp[p] = cpow_cs(z1, g0 - 1);
+      z[p] = cmul_cs(zp[p], z1);
     }
-    if (!LEVEL0) {
-      const float2* zf = zf_base + (long long)k * P.fine.kstride_z;
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        const float2* rp = zf + (long long)yf[t] * P.fine.pitch;
-        if (fvec_ok) {
-          d.f[2 * t] = ldg4(rp + xf0);
-          d.f[2 * t + 1] = ldg4(rp + xf0 + 2);
-        } else {
-          d.f[2 * t] = cat4(__ldg(rp + xf[0]), __ldg(rp + xf[1]));
-          d.f[2 * t + 1] = cat4(__ldg(rp + xf[2]), __ldg(rp + xf[3]));
-        }
-      }
-    }
-  };
+    acc[p] = make_float2(0.f, 0.f);
+  }
 
-  auto compute = [&](const KData& d, int k) {
-    // horizontal polyphase up-sampling of the 3 coarse rows (unscaled):
-    //   even fine col 2c: x_{c-1} + 6 x_c + x_{c+1} (/8); odd 2c+1: x_c + x_{c+1} (/2)
+  // ---- order loop
+#pragma unroll 1
+  for (int k = 0; k < KL; ++k) {
+    const int s = k % S;
+    mbar_wait_parity(&full[s], (k / S) & 1);
+    const unsigned char* st = smem + s * STAGE;
     float2 h[3][4];
 #pragma unroll
     for (int t = 0; t < 3; ++t) {
-      const float2 x0 = lo2(d.q[t]), x1 = hi2(d.q[t]);
+      const float4 qv = *reinterpret_cast<const float4*>(st + (warp + t) * CROW_BYTES + lane * 16);
+      const float2 x0 = lo2(qv), x1 = hi2(qv);
       const float2 L = shfl_up2(x1), Rn = shfl_down2(x0);
+      // horizontal polyphase (unscaled): even fine col x_{c-1} + 6 x_c + x_{c+1} (/8), odd x_c + x_{c+1} (/2)
       h[t][0] = pfma(bc(6.f), x0, padd(L, x1));
       h[t][1] = padd(x0, x1);
       h[t][2] = pfma(bc(6.f), x1, padd(x0, Rn));
       h[t][3] = padd(x1, Rn);
+    }
+    float4 fz[4];
+    if (!LEVEL0) {
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const unsigned char* fr = st + FOFF + (2 * warp + t) * FROW_BYTES + lane * 32;
+        fz[2 * t] = *reinterpret_cast<const float4*>(fr);
+        fz[2 * t + 1] = *reinterpret_cast<const float4*>(fr + 16);
+      }
     }
     float2 waa, w1, w2, w3;
     if (MAPS) {
@@ -503,6 +575,8 @@ __global__ void __launch_bounds__(128) k_apply(const ApplyParams P) {
     } else {
       waa = P.wk[k][0]; w1 = P.wk[k][1]; w2 = P.wk[k][2]; w3 = P.wk[k][3];
     }
+    const float kk = (float)(P.kbase + k);
+    const float kratio = (kk + 1.f) / kk;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       // vertical: even fine row (h[-1] + 6 h[0] + h[+1]) (/8); odd (h[0] + h[+1]) (/2)
@@ -518,7 +592,7 @@ __global__ void __launch_bounds__(128) k_apply(const ApplyParams P) {
         float2 V;  // (Im, Re) of a_k (Z_l - up Z_{l+1}) at this pixel
         float2 zf = make_float2(0.f, 0.f);
         if (!LEVEL0) {
-          const float4 fv = d.f[2 * t + (q >> 1)];
+          const float4 fv = fz[2 * t + (q >> 1)];
           zf = (q & 1) ? hi2(fv) : lo2(fv);
         }
         if (MAPS) {
@@ -526,53 +600,24 @@ __global__ void __launch_bounds__(128) k_apply(const ApplyParams P) {
         } else {
           V = LEVEL0 ? pmul(w, raw) : pfma(w, raw, pmul(waa, zf));
         }
-        // acc += (c V.im, s V.re); result = acc.x - acc.y = a Im(e^{-i k w g} (...))
+        // acc += (c V.im, s V.re); result = acc.x - acc.y = a_k Im(e^{-i k w_1 g} (...))
         acc[p] = pfma(z[p], V, acc[p]);
-        const float2 zn = pfma(tc[p], z[p], pneg(zp[p]));
+        const float2 zn = pfma(bc(-1.f), zp[p], pmul(bc(tc[p]), z[p]));
         zp[p] = z[p];
         z[p] = zn;
         if (MAPS) {
-          // a_{k+1} = a_k (k+1)/k exp(-(2k+1) beta)
-          const float kk = (float)(P.kbase + k);
-          mA[p] *= mR[p] * ((kk + 1.f) / kk);
+          mA[p] *= mR[p] * kratio;
           mR[p] *= mQ[p];
         }
       }
     }
-  };
-
-  {
-    KData A, B;
-    int k = k_lo;
-    if (k < k_hi) loadk(k, A);
-#pragma unroll 1
-    while (k < k_hi) {
-      if (k + 1 < k_hi) loadk(k + 1, B);
-      compute(A, k);
-      if (k + 1 >= k_hi) break;
-      if (k + 2 < k_hi) loadk(k + 2, A);
-      compute(B, k + 1);
-      k += 2;
-    }
+    __syncthreads();  // every warp is done with slot s
+    if (tid == 0 && k + S < KL) issue(k + S);
   }
 
   float res[8];
 #pragma unroll
   for (int p = 0; p < 8; ++p) res[p] = acc[p].x - acc[p].y;
-
-  if (KSPLIT > 1) {
-    __shared__ float red[KSPLIT > 1 ? KSPLIT - 1 : 1][8][32];
-    if (warp > 0) {
-#pragma unroll
-      for (int p = 0; p < 8; ++p) red[warp - 1][p][lane] = res[p];
-    }
-    __syncthreads();
-    if (warp > 0) return;
-#pragma unroll
-    for (int w = 0; w < KSPLIT - 1; ++w)
-#pragma unroll
-      for (int p = 0; p < 8; ++p) res[p] += red[w][p][lane];
-  }
 
   // --- collapse: + up(D_{l+1})
   if (HAS_D) {
@@ -626,69 +671,73 @@ __global__ void __launch_bounds__(128) k_apply(const ApplyParams P) {
 }
 
 // Rows per warp strip: long strips amortise the 3 halo rows; shorter strips
-// when the grid would not fill the GPU.
+// only when the grid would leave SMs without warps.
 int pick_rows(int Hc, int blocks_x, int z) {
   int R = 16;
-  while (R > 2 && (long long)blocks_x * ((Hc + R - 1) / R) * z < 148LL * 4) R >>= 1;
+  while (R > 2 && (long long)blocks_x * ((Hc + R - 1) / R) * z < 148LL * 8) R >>= 1;
   return R;
 }
 
 }  // namespace
 
+template <int NC, bool FROM_IMAGE>
+static cudaError_t launch_build_nc(BuildParams p, int batch, cudaStream_t s) {
+  const int bx = (p.Wc + 29) / 30;  // one warp (CTA) per 30 coarse columns
+  p.nchunks = p.KL / NC;
+  p.rows_per_strip = pick_rows(p.Hc, bx, batch * p.nchunks);
+  dim3 grid(bx, (p.Hc + p.rows_per_strip - 1) / p.rows_per_strip, batch * p.nchunks);
+  k_build<NC, 1, FROM_IMAGE><<<grid, 32, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+// largest channel chunk (<= cap) dividing the local order count
+static int chunk_for(int KL, int cap) {
+  for (int c = cap; c > 1; --c)
+    if (KL % c == 0) return c;
+  return 1;
+}
+
 cudaError_t launch_build(const BuildParams& p0, int level_src, int batch, cudaStream_t s) {
   BuildParams p = p0;
-  const int warps_x = (p.Wc + 29) / 30;
-  const int bx = (warps_x + 3) / 4;
   if (p.maps) {
+    const int bx = (p.Wc + 29) / 30;
     p.nchunks = 1;
     p.rows_per_strip = pick_rows(p.Hc, bx, 1);
     dim3 grid(bx, (p.Hc + p.rows_per_strip - 1) / p.rows_per_strip, 1);
     if (level_src == 0)
-      k_build<0, 2, true><<<grid, 128, 0, s>>>(p);
+      k_build<0, 2, true><<<grid, 32, 0, s>>>(p);
     else
-      k_build<0, 2, false><<<grid, 128, 0, s>>>(p);
+      k_build<0, 2, false><<<grid, 32, 0, s>>>(p);
     return cudaGetLastError();
   }
   if (level_src == 0) {
-    if (p.KL <= 4) {
-      p.nchunks = 1;
-      p.rows_per_strip = pick_rows(p.Hc, bx, batch);
-      dim3 grid(bx, (p.Hc + p.rows_per_strip - 1) / p.rows_per_strip, batch);
-      k_build<4, 1, true><<<grid, 128, 0, s>>>(p);
-    } else {
-      constexpr int NC = 8;
-      p.nchunks = (p.KL + NC - 1) / NC;
-      p.rows_per_strip = pick_rows(p.Hc, bx, batch * p.nchunks);
-      dim3 grid(bx, (p.Hc + p.rows_per_strip - 1) / p.rows_per_strip, batch * p.nchunks);
-      k_build<NC, 1, true><<<grid, 128, 0, s>>>(p);
+    switch (chunk_for(p.KL, 6)) {
+      case 6: return launch_build_nc<6, true>(p, batch, s);
+      case 5: return launch_build_nc<5, true>(p, batch, s);
+      case 4: return launch_build_nc<4, true>(p, batch, s);
+      case 3: return launch_build_nc<3, true>(p, batch, s);
+      case 2: return launch_build_nc<2, true>(p, batch, s);
+      default: return launch_build_nc<1, true>(p, batch, s);
     }
-  } else {
-    constexpr int NC = 2;
-    p.nchunks = (p.KL + NC - 1) / NC;
-    p.rows_per_strip = pick_rows(p.Hc, bx, batch * p.nchunks);
-    dim3 grid(bx, (p.Hc + p.rows_per_strip - 1) / p.rows_per_strip, batch * p.nchunks);
-    k_build<NC, 1, false><<<grid, 128, 0, s>>>(p);
   }
-  return cudaGetLastError();
+  switch (chunk_for(p.KL, 3)) {
+    case 3: return launch_build_nc<3, false>(p, batch, s);
+    case 2: return launch_build_nc<2, false>(p, batch, s);
+    default: return launch_build_nc<1, false>(p, batch, s);
+  }
 }
 
 template <bool L0, bool HD, bool MP>
-static void launch_apply_t(const ApplyParams& p, int batch, cudaStream_t s) {
-  const int pairs = (p.Wc + 1) / 2;
-  const int warps_x = (pairs + 29) / 30;
-  const long long ctas1 = (long long)((warps_x + 3) / 4) * p.Hc * batch;
-  if (ctas1 >= 2 * 148 || p.KL < 4) {
-    dim3 grid((warps_x + 3) / 4, p.Hc, batch);
-    k_apply<L0, HD, MP, 1><<<grid, 128, 0, s>>>(p);
-  } else {
-    dim3 grid(warps_x, p.Hc, batch);
-    k_apply<L0, HD, MP, 4><<<grid, 128, 0, s>>>(p);
-  }
+static cudaError_t launch_apply_t(const ApplyParams& p, int batch, cudaStream_t s) {
+  dim3 grid((p.Wf + 119) / 120, (p.Hc + 3) / 4, batch);
+  const int smem = APPLY_STAGES * apply_stage_bytes<L0>();
+  k_apply<L0, HD, MP><<<grid, 128, smem, s>>>(p);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_apply(const ApplyParams& p, int level_fine, bool has_d, bool maps, int batch,
                          cudaStream_t s) {
-#define FLLF_APPLY(L0, HD, MP) launch_apply_t<L0, HD, MP>(p, batch, s)
+#define FLLF_APPLY(L0, HD, MP) return launch_apply_t<L0, HD, MP>(p, batch, s)
   if (level_fine == 0) {
     if (maps) {
       if (has_d) FLLF_APPLY(true, true, true); else FLLF_APPLY(true, false, true);
@@ -703,7 +752,6 @@ cudaError_t launch_apply(const ApplyParams& p, int level_fine, bool has_d, bool 
     }
   }
 #undef FLLF_APPLY
-  return cudaGetLastError();
 }
 
 }  // namespace fllf
