@@ -37,6 +37,9 @@ WORKLOADS = {
                                           "T=510, sigma_r=30, m=3; 1 frame per rank per step"),
     "config5": dict(cfg=5, frames=64, desc="BASELINE configs[4]: 64 frames 1080x1920 gray, 6 levels, K=16, "
                                            "T=510, sigma_r=30, m=3; 64/N frames per rank per step"),
+    "config3": dict(cfg=3, frames=1, desc="BASELINE configs[2]: 2160x3840 RGB (per channel), 7 levels, K=10, "
+                                          "T=510, sigma_r=20, m=2; (channel, order) units sharded over N ranks, "
+                                          "partial collapse + one NCCL reduce per channel to rank 0"),
 }
 
 
@@ -184,6 +187,74 @@ def run_reference(args):
     return 0
 
 
+# ------------------------------------------------------------ config 3
+def run_sharded(args, c, wl, world, rank, local):
+    """Order-sharded 4K RGB: units (channel, order) split over ranks, partial
+    collapse per rank, NCCL reduce (sum) per channel to rank 0."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2206_04681_b200 import dist as D
+    from paper_2206_04681_b200 import fllf as F
+    from paper_2206_04681_b200 import synth
+
+    H, W, levels, K = c["H"], c["W"], c["levels"], c["K"]
+    if world == 1:
+        # the reduce of a single rank is the identity; use a 1-rank gloo group for the same code path
+        import socket
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(s.getsockname()[1]))
+        s.close()
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", local))
+    rgb = synth.config3_rgb()
+    img = torch.from_numpy(rgb).cuda()
+    out = torch.empty_like(img)
+    fn = D.gpu_partial_fn(img, levels, K, c["T"], c["sigma_r"], c["m"])
+    l2 = torch.cuda.get_device_properties(local).L2_cache_size or 126 * 2 ** 20
+    flush_buf = torch.empty(2 * l2 // 4 + 1024, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+    for _ in range(max(args.warmup, 1)):
+        flush_buf.zero_()
+        D.sharded_filter(fn, out, 3, K)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk = ClockSampler(local)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    launches = 0
+    clk.start()
+    for i in range(args.steps):
+        flush_buf.zero_()
+        starts[i].record(stream)
+        D.sharded_filter(fn, out, 3, K)
+        ends[i].record(stream)
+        launches += sum(p.launches for p in fn.plans.values())
+    torch.cuda.synchronize()
+    clk.stop()
+    dist.barrier()
+    t = torch.tensor([sum(a.elapsed_time(b) for a, b in zip(starts, ends))], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tot_ms = float(t.item())
+    value = H * W * args.steps / 1e6 / (tot_ms / 1e3)
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot_ms / args.steps, 4),
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic",
+                "config": {"workload": wl["desc"], "H": H, "W": W, "channels": 3, "levels": levels, "K": K,
+                           "parallelism": f"order-shard{world}",
+                           "l2": f"flushed between timed steps ({flush_buf.numel() * 4 >> 20} MiB write)"},
+                "gpu_launches": launches, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    clk.close()
+    for p in fn.plans.values():
+        p.close()
+    dist.destroy_process_group()
+    return 0
+
+
 # ------------------------------------------------------------------- main
 def main():
     ap = argparse.ArgumentParser()
@@ -214,6 +285,8 @@ def main():
     wl = WORKLOADS[args.workload]
     c = synth.CONFIGS[wl["cfg"]]
     H, W, levels, K = c["H"], c["W"], c["levels"], c["K"]
+    if wl["cfg"] == 3:
+        return run_sharded(args, c, wl, world, rank, local)
     if wl["cfg"] == 2:
         frames = 1
         imgs = np.stack([synth.config2_image(seed=2000 + rank)])

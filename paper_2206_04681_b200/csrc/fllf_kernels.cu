@@ -91,6 +91,15 @@ __device__ __forceinline__ void sincos_turns(float val, float invT, float* s, fl
   __sincosf(TWO_PI * u, s, c);
 }
 
+// e^{i n theta}: n * frac(val/T) reduced again to [-1/2, 1/2] turns.
+__device__ __forceinline__ void sincos_turns_n(float val, float invT, int n, float* s, float* c) {
+  float u = val * invT;
+  u -= rintf(u);
+  u *= (float)n;
+  u -= rintf(u);
+  __sincosf(TWO_PI * u, s, c);
+}
+
 // complex products for unit phasors.  (s, c) layout = (Im, Re).
 __device__ __forceinline__ float2 cmul_sc(float2 a, float2 b) {
   return make_float2(fmaf(a.x, b.y, a.y * b.x), fmaf(a.y, b.y, -a.x * b.x));
@@ -99,26 +108,6 @@ __device__ __forceinline__ float2 cmul_sc(float2 a, float2 b) {
 __device__ __forceinline__ float2 cmul_cs(float2 a, float2 b) {
   return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
 }
-// z^n by binary powering (n >= 0, warp-uniform); identity is (0,1) / (1,0).
-__device__ __forceinline__ float2 cpow_sc(float2 z, int n) {
-  float2 r = make_float2(0.f, 1.f);
-  while (n) {
-    if (n & 1) r = cmul_sc(r, z);
-    z = cmul_sc(z, z);
-    n >>= 1;
-  }
-  return r;
-}
-__device__ __forceinline__ float2 cpow_cs(float2 z, int n) {
-  float2 r = make_float2(1.f, 0.f);
-  while (n) {
-    if (n & 1) r = cmul_cs(r, z);
-    z = cmul_cs(z, z);
-    n >>= 1;
-  }
-  return r;
-}
-
 __device__ __forceinline__ float2 ldg2(const float* p) { return __ldg(reinterpret_cast<const float2*>(p)); }
 __device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 __device__ __forceinline__ float4 ldg4(const float2* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
@@ -304,8 +293,12 @@ struct BuildWarp {
           zp[q] = make_float2(0.f, 1.f);
           zc[q] = z1;
         } else {
-          zp[q] = cpow_sc(z1, g0 - 1);
-          zc[q] = cmul_sc(zp[q], z1);
+          // chunk start: e^{i g0 theta} directly (range-reduced in turns),
+          // e^{i (g0-1) theta} = e^{i g0 theta} e^{-i theta}
+          float sg, cg;
+          sincos_turns_n(I4[q], P.invT, g0, &sg, &cg);
+          zc[q] = make_float2(sg, cg);
+          zp[q] = make_float2(fmaf(sg, cs, -cg * sn), fmaf(cg, cs, sg * sn));
         }
       }
 #pragma unroll
@@ -387,13 +380,16 @@ __host__ __device__ constexpr int apply_stage_bytes() {
   return 6 * CROW_BYTES + (LEVEL0 ? 0 : 8 * FROW_BYTES);
 }
 
+// Warp-specialised: warps 0..3 compute (one coarse row each), warp 4 is the
+// TMA producer that refills a stage as soon as the 4 consumer warps released it.
 template <bool LEVEL0, bool HAS_D, bool MAPS>
-__global__ void __launch_bounds__(128, 3) k_apply(const ApplyParams P) {
+__global__ void __launch_bounds__(160, 3) k_apply(const ApplyParams P) {
   constexpr int S = APPLY_STAGES;
   constexpr int STAGE = apply_stage_bytes<LEVEL0>();
   constexpr int FOFF = 6 * CROW_BYTES;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t full[S];
+  __shared__ __align__(8) uint64_t empty[S];
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -414,32 +410,38 @@ __global__ void __launch_bounds__(128, 3) k_apply(const ApplyParams P) {
   const float2* zf0 = LEVEL0 ? nullptr : P.fine.Z + frame * P.fine.fstride_z + (120 * jb - 4);
   if (tid == 0) {
 #pragma unroll
-    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 4);
+    }
     fence_mbar_init();
   }
   __syncthreads();
-  auto issue = [&](int k) {
-    const int s = k % S;
-    unsigned char* st = smem + s * STAGE;
-    mbar_arrive_expect_tx(&full[s], STAGE);
-    const float2* zc = zc0 + (long long)k * P.coarse.kstride_z;
+  if (warp == 4) {
+    // ---- producer warp: one elected lane issues all bulk copies
+    if (lane == 0) {
+      for (int k = 0; k < KL; ++k) {
+        const int s = k % S;
+        if (k >= S) mbar_wait_parity(&empty[s], ((k / S) - 1) & 1);
+        unsigned char* st = smem + s * STAGE;
+        mbar_arrive_expect_tx(&full[s], STAGE);
+        const float2* zc = zc0 + (long long)k * P.coarse.kstride_z;
 #pragma unroll
-    for (int t = 0; t < 6; ++t) {
-      const int cr = upmap(r0 - 1 + t, P.Hc, P.Hf);
-      tma_load_1d(st + t * CROW_BYTES, zc + (long long)cr * P.coarse.zpitch, CROW_BYTES, &full[s]);
-    }
-    if (!LEVEL0) {
-      const float2* zf = zf0 + (long long)k * P.fine.kstride_z;
+        for (int t = 0; t < 6; ++t) {
+          const int cr = upmap(r0 - 1 + t, P.Hc, P.Hf);
+          tma_load_1d(st + t * CROW_BYTES, zc + (long long)cr * P.coarse.zpitch, CROW_BYTES, &full[s]);
+        }
+        if (!LEVEL0) {
+          const float2* zf = zf0 + (long long)k * P.fine.kstride_z;
 #pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        const int fr = min(2 * r0 + t, P.Hf - 1);
-        tma_load_1d(st + FOFF + t * FROW_BYTES, zf + (long long)fr * P.fine.zpitch, FROW_BYTES, &full[s]);
+          for (int t = 0; t < 8; ++t) {
+            const int fr = min(2 * r0 + t, P.Hf - 1);
+            tma_load_1d(st + FOFF + t * FROW_BYTES, zf + (long long)fr * P.fine.zpitch, FROW_BYTES, &full[s]);
+          }
+        }
       }
     }
-  };
-  if (tid == 0) {
-    const int npre = KL < S ? KL : S;
-    for (int k = 0; k < npre; ++k) issue(k);
+    return;
   }
 
   // ---- per-thread setup (overlaps the first copies)
@@ -536,8 +538,10 @@ __global__ void __launch_bounds__(128, 3) k_apply(const ApplyParams P) {
       zp[p] = make_float2(1.f, 0.f);
       z[p] = z1;
     } else {
-      zp[p] = cpow_cs(z1, g0 - 1);
-      z[p] = cmul_cs(zp[p], z1);
+      float sg, cg;
+      sincos_turns_n(g[p], P.invT, g0, &sg, &cg);
+      z[p] = make_float2(cg, sg);
+      zp[p] = make_float2(fmaf(cg, cs, sg * sn), fmaf(sg, cs, -cg * sn));
     }
     acc[p] = make_float2(0.f, 0.f);
   }
@@ -611,8 +615,8 @@ __global__ void __launch_bounds__(128, 3) k_apply(const ApplyParams P) {
         }
       }
     }
-    __syncthreads();  // every warp is done with slot s
-    if (tid == 0 && k + S < KL) issue(k + S);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with slot s
   }
 
   float res[8];
@@ -711,7 +715,9 @@ cudaError_t launch_build(const BuildParams& p0, int level_src, int batch, cudaSt
     return cudaGetLastError();
   }
   if (level_src == 0) {
-    switch (chunk_for(p.KL, 6)) {
+    switch (chunk_for(p.KL, 8)) {
+      case 8: return launch_build_nc<8, true>(p, batch, s);
+      case 7: return launch_build_nc<7, true>(p, batch, s);
       case 6: return launch_build_nc<6, true>(p, batch, s);
       case 5: return launch_build_nc<5, true>(p, batch, s);
       case 4: return launch_build_nc<4, true>(p, batch, s);
@@ -720,7 +726,8 @@ cudaError_t launch_build(const BuildParams& p0, int level_src, int batch, cudaSt
       default: return launch_build_nc<1, true>(p, batch, s);
     }
   }
-  switch (chunk_for(p.KL, 3)) {
+  switch (chunk_for(p.KL, 4)) {
+    case 4: return launch_build_nc<4, false>(p, batch, s);
     case 3: return launch_build_nc<3, false>(p, batch, s);
     case 2: return launch_build_nc<2, false>(p, batch, s);
     default: return launch_build_nc<1, false>(p, batch, s);
@@ -731,7 +738,7 @@ template <bool L0, bool HD, bool MP>
 static cudaError_t launch_apply_t(const ApplyParams& p, int batch, cudaStream_t s) {
   dim3 grid((p.Wf + 119) / 120, (p.Hc + 3) / 4, batch);
   const int smem = APPLY_STAGES * apply_stage_bytes<L0>();
-  k_apply<L0, HD, MP><<<grid, 128, smem, s>>>(p);
+  k_apply<L0, HD, MP><<<grid, 160, smem, s>>>(p);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,87 @@
+"""Multi-process host logic of the multi-GPU drivers, on CPU with gloo
+(world size 2, 127.0.0.1).  The per-unit compute is the fp64 oracle here (test
+infrastructure); on GPU it is a libfllf plan (paper_2206_04681_b200.dist.gpu_partial_fn)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2206_04681_b200.dist import Segment, frame_partition, order_partition, sharded_filter
+
+
+def test_frame_partition_covers_all():
+    for n in (1, 7, 64):
+        for world in (1, 2, 3, 8):
+            seen = []
+            for r in range(world):
+                f, c = frame_partition(n, world, r)
+                seen += list(range(f, f + c))
+                assert abs(c - n / world) < 1
+            assert seen == list(range(n))
+
+
+@pytest.mark.parametrize("C,K", [(3, 10), (1, 8), (3, 1), (2, 16)])
+@pytest.mark.parametrize("world", [1, 2, 4, 8, 13])
+def test_order_partition_properties(C, K, world):
+    parts = order_partition(C, K, world)
+    units = [(s.channel, k) for segs in parts for s in segs for k in range(s.k_begin, s.k_end)]
+    assert sorted(units) == [(c, k) for c in range(C) for k in range(1, K + 1)]
+    sizes = [sum(s.k_end - s.k_begin for s in segs) for segs in parts]
+    assert max(sizes) - min(sizes) <= 1
+    for c in range(C):
+        assert sum(1 for segs in parts for s in segs if s.channel == c and s.include_base) == 1
+    for segs in parts:                       # at most one range per channel per rank
+        chans = [s.channel for s in segs]
+        assert len(chans) == len(set(chans))
+
+
+def test_config3_balance_at_8():
+    parts = order_partition(3, 10, 8)       # 30 units -> 4,4,4,4,4,4,3,3
+    assert sorted(sum(s.k_end - s.k_begin for s in p) for p in parts) == [3, 3, 4, 4, 4, 4, 4, 4]
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, img, args, result_path):
+    from oracle import fllf_oracle as O
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    levels, K, T, sig, m = args
+    C, H, W = img.shape
+    out = torch.zeros((C, H, W), dtype=torch.float64)
+
+    def partial_fn(seg: Segment, out_c):
+        part = O.fourier_llf(img[seg.channel], levels, K, T, sig, m, k_range=(seg.k_begin, seg.k_end),
+                             include_base=False)
+        if seg.include_base:
+            part = part + img[seg.channel]
+        out_c.copy_(torch.from_numpy(part))
+
+    sharded_filter(partial_fn, out, C, K)
+    if rank == 0:
+        np.save(result_path, out.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_sharded_filter_gloo_equals_full(tmp_path, world):
+    rng = np.random.default_rng(3)
+    img = rng.uniform(0, 255, (3, 24, 21))
+    args = (3, 5, 510.0, 20.0, 2.0)
+    res = str(tmp_path / "out.npy")
+    mp.spawn(_worker, args=(world, _free_port(), img, args, res), nprocs=world, join=True)
+    from oracle import fllf_oracle as O
+    full = np.stack([O.fourier_llf(img[c], *args) for c in range(3)])
+    assert np.abs(np.load(res) - full).max() <= 1e-9
