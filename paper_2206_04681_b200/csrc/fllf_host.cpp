@@ -78,6 +78,7 @@ struct fllf_plan_s {
   // CUDA graph of the whole filter sequence (build + apply), replayed on the
   // caller's stream; re-captured when the buffers or the profiling flag change
   bool use_graph = true;
+  bool use_pdl = true;  // programmatic dependent launch between the kernels of a sequence
   bool capturing = false;
   cudaStream_t cap_stream = nullptr;
   cudaGraphExec_t gexec = nullptr;
@@ -196,6 +197,8 @@ fllf_status fllf_plan_create_ex(const fllf_plan_desc* din, fllf_plan* out) {
   {
     const char* ng = std::getenv("FLLF_NO_GRAPH");
     p->use_graph = !(ng && ng[0] == '1');
+    const char* np = std::getenv("FLLF_NO_PDL");
+    p->use_pdl = !(np && np[0] == '1');
   }
   int dev = d.device;
   if (dev < 0) {
@@ -329,7 +332,7 @@ fllf_status fllf_build_fourier_pyramids(fllf_plan p, const float* d_img, size_t 
     cudaError_t e;
     {
       ProfScope ps(p, stream, l == 0 ? FLLF_K_BUILD0 : FLLF_K_BUILD, l);
-      e = fllf::launch_build(bp, l, p->d.batch, stream);
+      e = fllf::launch_build(bp, l, p->d.batch, stream, p->use_pdl && l > 0);
     }
     if (e != cudaSuccess) return cuda_fail(e, "build kernel launch");
     ++launches;
@@ -450,7 +453,7 @@ fllf_status fllf_apply(fllf_plan p, const fllf_apply_args* a, float* d_out, size
       cudaError_t e;
       {
         ProfScope ps(p, stream, FLLF_K_MAPBUILD, l);
-        e = fllf::launch_build(bp, l, 1, stream);
+        e = fllf::launch_build(bp, l, 1, stream, false);
       }
       if (e != cudaSuccess) return cuda_fail(e, "map pyramid kernel launch");
       ++launches;
@@ -465,10 +468,11 @@ fllf_status fllf_apply(fllf_plan p, const fllf_apply_args* a, float* d_out, size
     ap.Hc = p->Hs[l + 1];
     ap.Wc = p->Ws[l + 1];
     const bool has_d = (l + 1) < lmax;  // D_lmax = 0
+    ap.wait_first = (l == lmax - 1) ? 1 : 0;
     cudaError_t e;
     {
       ProfScope ps(p, stream, l == 0 ? FLLF_K_APPLY0 : FLLF_K_APPLY, l);
-      e = fllf::launch_apply(ap, l, has_d, maps, p->d.batch, stream);
+      e = fllf::launch_apply(ap, l, has_d, maps, p->d.batch, stream, p->use_pdl);
     }
     if (e != cudaSuccess) return cuda_fail(e, "apply kernel launch");
     ++launches;

@@ -67,6 +67,7 @@ struct ApplyParams {
   int Hf, Wf, Hc, Wc;
   int KL, kbase;
   int include_base;
+  int wait_first;      // PDL: wait for the preceding grid before any global read
   float invT;          // 1/T
   float c0;            // MAPS: 2 omega_1 sqrt(2 pi) / T
   float hq;            // MAPS: omega_1^2 / 2
@@ -79,8 +80,10 @@ struct ApplyParams {
 };
 
 // Kernel launchers (fllf_kernels.cu).  Return cudaGetLastError() after launch.
-cudaError_t launch_build(const BuildParams& p, int level_src, int batch, cudaStream_t s);
+// pdl: launch with programmatic stream serialization (the kernel may start
+// while its predecessor is still running; it synchronises with griddepcontrol)
+cudaError_t launch_build(const BuildParams& p, int level_src, int batch, cudaStream_t s, bool pdl);
 cudaError_t launch_apply(const ApplyParams& p, int level_fine, bool has_d, bool maps, int batch,
-                         cudaStream_t s);
+                         cudaStream_t s, bool pdl);
 
 }  // namespace fllf

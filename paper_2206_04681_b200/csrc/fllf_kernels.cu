@@ -348,6 +348,8 @@ struct BuildWarp {
 
 template <int NC, int NR, bool FROM_IMAGE>
 __global__ void __launch_bounds__(32) k_build(const BuildParams P) {
+  pdl_wait();     // the previous level's planes are complete
+  pdl_trigger();  // let the next kernel get scheduled
   const int cb = blockIdx.x;  // one warp per CTA: all control flow is blockIdx-uniform
   if (cb * 30 >= P.Wc) return;
   const int o0 = blockIdx.y * P.rows_per_strip;
@@ -383,7 +385,7 @@ __host__ __device__ constexpr int apply_stage_bytes() {
 // Warp-specialised: warps 0..3 compute (one coarse row each), warp 4 is the
 // TMA producer that refills a stage as soon as the 4 consumer warps released it.
 template <bool LEVEL0, bool HAS_D, bool MAPS>
-__global__ void __launch_bounds__(160, 3) k_apply(const ApplyParams P) {
+__global__ void __launch_bounds__(160, 2) k_apply(const ApplyParams P) {
   constexpr int S = APPLY_STAGES;
   constexpr int STAGE = apply_stage_bytes<LEVEL0>();
   constexpr int FOFF = 6 * CROW_BYTES;
@@ -391,6 +393,11 @@ __global__ void __launch_bounds__(160, 3) k_apply(const ApplyParams P) {
   __shared__ __align__(8) uint64_t full[S];
   __shared__ __align__(8) uint64_t empty[S];
 
+  // PDL: the Z / G planes of the build pass are complete once the first apply
+  // of the sequence has waited; only D_{l+1} (previous apply) needs a wait,
+  // taken right before it is read after the order loop.
+  if (P.wait_first) pdl_wait();
+  pdl_trigger();
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
@@ -456,22 +463,6 @@ __global__ void __launch_bounds__(160, 3) k_apply(const ApplyParams P) {
   const bool cvec = (2 * j >= 0) && (2 * j + 1 < P.Wc);
   const int cc0 = upmap(2 * j, P.Wc, P.Wf), cc1 = upmap(2 * j + 1, P.Wc, P.Wf);
 
-  float dq[3][2];
-  if (HAS_D) {
-    const float* dc = P.coarse.D + frame * P.coarse.fstride_r;
-#pragma unroll
-    for (int t = 0; t < 3; ++t) {
-      const float* rp = dc + (long long)cr[t] * P.coarse.pitch;
-      if (cvec) {
-        const float2 q = ldg2(rp + 2 * j);
-        dq[t][0] = q.x;
-        dq[t][1] = q.y;
-      } else {
-        dq[t][0] = __ldg(rp + cc0);
-        dq[t][1] = __ldg(rp + cc1);
-      }
-    }
-  }
   float g[8];
   {
     const float* base;
@@ -546,8 +537,8 @@ __global__ void __launch_bounds__(160, 3) k_apply(const ApplyParams P) {
     acc[p] = make_float2(0.f, 0.f);
   }
 
-  // ---- order loop
-#pragma unroll 1
+  // ---- order loop (unrolled by 2 so the recurrence state rotates without moves)
+#pragma unroll 2
   for (int k = 0; k < KL; ++k) {
     const int s = k % S;
     mbar_wait_parity(&full[s], (k / S) & 1);
@@ -623,8 +614,23 @@ __global__ void __launch_bounds__(160, 3) k_apply(const ApplyParams P) {
 #pragma unroll
   for (int p = 0; p < 8; ++p) res[p] = acc[p].x - acc[p].y;
 
-  // --- collapse: + up(D_{l+1})
+  // --- collapse: + up(D_{l+1}) (written by the previous apply grid)
   if (HAS_D) {
+    pdl_wait();
+    float dq[3][2];
+    const float* dc = P.coarse.D + frame * P.coarse.fstride_r;
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      const float* rp = dc + (long long)cr[t] * P.coarse.pitch;
+      if (cvec) {
+        const float2 q = ldg2(rp + 2 * j);
+        dq[t][0] = q.x;
+        dq[t][1] = q.y;
+      } else {
+        dq[t][0] = __ldg(rp + cc0);
+        dq[t][1] = __ldg(rp + cc1);
+      }
+    }
     float hd[3][4];
 #pragma unroll
     for (int t = 0; t < 3; ++t) {
@@ -674,6 +680,21 @@ __global__ void __launch_bounds__(160, 3) k_apply(const ApplyParams P) {
   }
 }
 
+template <typename Kern, typename Par>
+cudaError_t launch_ex(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl, const Par& p) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, p);
+}
+
 // Rows per warp strip: long strips amortise the 3 halo rows; shorter strips
 // only when the grid would leave SMs without warps.
 int pick_rows(int Hc, int blocks_x, int z) {
@@ -685,13 +706,12 @@ int pick_rows(int Hc, int blocks_x, int z) {
 }  // namespace
 
 template <int NC, bool FROM_IMAGE>
-static cudaError_t launch_build_nc(BuildParams p, int batch, cudaStream_t s) {
+static cudaError_t launch_build_nc(BuildParams p, int batch, cudaStream_t s, bool pdl) {
   const int bx = (p.Wc + 29) / 30;  // one warp (CTA) per 30 coarse columns
   p.nchunks = p.KL / NC;
   p.rows_per_strip = pick_rows(p.Hc, bx, batch * p.nchunks);
   dim3 grid(bx, (p.Hc + p.rows_per_strip - 1) / p.rows_per_strip, batch * p.nchunks);
-  k_build<NC, 1, FROM_IMAGE><<<grid, 32, 0, s>>>(p);
-  return cudaGetLastError();
+  return launch_ex(k_build<NC, 1, FROM_IMAGE>, grid, dim3(32), 0, s, pdl, p);
 }
 
 // largest channel chunk (<= cap) dividing the local order count
@@ -701,50 +721,46 @@ static int chunk_for(int KL, int cap) {
   return 1;
 }
 
-cudaError_t launch_build(const BuildParams& p0, int level_src, int batch, cudaStream_t s) {
+cudaError_t launch_build(const BuildParams& p0, int level_src, int batch, cudaStream_t s, bool pdl) {
   BuildParams p = p0;
   if (p.maps) {
     const int bx = (p.Wc + 29) / 30;
     p.nchunks = 1;
     p.rows_per_strip = pick_rows(p.Hc, bx, 1);
     dim3 grid(bx, (p.Hc + p.rows_per_strip - 1) / p.rows_per_strip, 1);
-    if (level_src == 0)
-      k_build<0, 2, true><<<grid, 32, 0, s>>>(p);
-    else
-      k_build<0, 2, false><<<grid, 32, 0, s>>>(p);
-    return cudaGetLastError();
+    if (level_src == 0) return launch_ex(k_build<0, 2, true>, grid, dim3(32), 0, s, pdl, p);
+    return launch_ex(k_build<0, 2, false>, grid, dim3(32), 0, s, pdl, p);
   }
   if (level_src == 0) {
     switch (chunk_for(p.KL, 8)) {
-      case 8: return launch_build_nc<8, true>(p, batch, s);
-      case 7: return launch_build_nc<7, true>(p, batch, s);
-      case 6: return launch_build_nc<6, true>(p, batch, s);
-      case 5: return launch_build_nc<5, true>(p, batch, s);
-      case 4: return launch_build_nc<4, true>(p, batch, s);
-      case 3: return launch_build_nc<3, true>(p, batch, s);
-      case 2: return launch_build_nc<2, true>(p, batch, s);
-      default: return launch_build_nc<1, true>(p, batch, s);
+      case 8: return launch_build_nc<8, true>(p, batch, s, pdl);
+      case 7: return launch_build_nc<7, true>(p, batch, s, pdl);
+      case 6: return launch_build_nc<6, true>(p, batch, s, pdl);
+      case 5: return launch_build_nc<5, true>(p, batch, s, pdl);
+      case 4: return launch_build_nc<4, true>(p, batch, s, pdl);
+      case 3: return launch_build_nc<3, true>(p, batch, s, pdl);
+      case 2: return launch_build_nc<2, true>(p, batch, s, pdl);
+      default: return launch_build_nc<1, true>(p, batch, s, pdl);
     }
   }
   switch (chunk_for(p.KL, 4)) {
-    case 4: return launch_build_nc<4, false>(p, batch, s);
-    case 3: return launch_build_nc<3, false>(p, batch, s);
-    case 2: return launch_build_nc<2, false>(p, batch, s);
-    default: return launch_build_nc<1, false>(p, batch, s);
+    case 4: return launch_build_nc<4, false>(p, batch, s, pdl);
+    case 3: return launch_build_nc<3, false>(p, batch, s, pdl);
+    case 2: return launch_build_nc<2, false>(p, batch, s, pdl);
+    default: return launch_build_nc<1, false>(p, batch, s, pdl);
   }
 }
 
 template <bool L0, bool HD, bool MP>
-static cudaError_t launch_apply_t(const ApplyParams& p, int batch, cudaStream_t s) {
+static cudaError_t launch_apply_t(const ApplyParams& p, int batch, cudaStream_t s, bool pdl) {
   dim3 grid((p.Wf + 119) / 120, (p.Hc + 3) / 4, batch);
   const int smem = APPLY_STAGES * apply_stage_bytes<L0>();
-  k_apply<L0, HD, MP><<<grid, 160, smem, s>>>(p);
-  return cudaGetLastError();
+  return launch_ex(k_apply<L0, HD, MP>, grid, dim3(160), smem, s, pdl, p);
 }
 
 cudaError_t launch_apply(const ApplyParams& p, int level_fine, bool has_d, bool maps, int batch,
-                         cudaStream_t s) {
-#define FLLF_APPLY(L0, HD, MP) return launch_apply_t<L0, HD, MP>(p, batch, s)
+                         cudaStream_t s, bool pdl) {
+#define FLLF_APPLY(L0, HD, MP) return launch_apply_t<L0, HD, MP>(p, batch, s, pdl)
   if (level_fine == 0) {
     if (maps) {
       if (has_d) FLLF_APPLY(true, true, true); else FLLF_APPLY(true, false, true);

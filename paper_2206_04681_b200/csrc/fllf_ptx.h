@@ -49,4 +49,11 @@ __device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src_gmem
       : "memory");
 }
 
+// Programmatic dependent launch (PDL).  wait: block until the preceding
+// grid in the stream has completed and its writes are visible (no-op when the
+// kernel was not launched with programmatic stream serialization);
+// launch_dependents: allow the next grid to be scheduled.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 }  // namespace fllf
