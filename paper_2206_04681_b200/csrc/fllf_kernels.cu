@@ -38,6 +38,7 @@
 // No tensor cores: this is a stencil + elementwise path (no contraction).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdlib>
 
 #include "fllf_internal.h"
 #include "fllf_ptx.h"
@@ -373,7 +374,12 @@ __global__ void __launch_bounds__(32) k_build(const BuildParams P) {
 }
 
 // ----------------------------------------------------------------- apply
-constexpr int APPLY_STAGES = 4;
+// TMA ring depth: enough stages in flight to cover the L2/HBM round trip
+// (level 0 stages are 3 KB, level >= 1 stages 11 KB)
+template <bool LEVEL0>
+__host__ __device__ constexpr int apply_stages() {
+  return LEVEL0 ? 8 : 6;
+}
 constexpr int CROW_BYTES = 64 * 8;   // 32 lanes x 2 coarse complex values
 constexpr int FROW_BYTES = 128 * 8;  // 32 lanes x 4 fine complex values
 
@@ -385,8 +391,8 @@ __host__ __device__ constexpr int apply_stage_bytes() {
 // Warp-specialised: warps 0..3 compute (one coarse row each), warp 4 is the
 // TMA producer that refills a stage as soon as the 4 consumer warps released it.
 template <bool LEVEL0, bool HAS_D, bool MAPS>
-__global__ void __launch_bounds__(160, 2) k_apply(const ApplyParams P) {
-  constexpr int S = APPLY_STAGES;
+__global__ void __launch_bounds__(160, MAPS ? 2 : 3) k_apply(const ApplyParams P) {
+  constexpr int S = apply_stages<LEVEL0>();
   constexpr int STAGE = apply_stage_bytes<LEVEL0>();
   constexpr int FOFF = 6 * CROW_BYTES;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -732,7 +738,12 @@ cudaError_t launch_build(const BuildParams& p0, int level_src, int batch, cudaSt
     return launch_ex(k_build<0, 2, false>, grid, dim3(32), 0, s, pdl, p);
   }
   if (level_src == 0) {
-    switch (chunk_for(p.KL, 8)) {
+    static const int cap0 = [] {
+      const char* e = std::getenv("FLLF_BUILD0_CHUNK");
+      const int v = e ? std::atoi(e) : 8;
+      return v >= 1 && v <= 8 ? v : 8;
+    }();
+    switch (chunk_for(p.KL, cap0)) {
       case 8: return launch_build_nc<8, true>(p, batch, s, pdl);
       case 7: return launch_build_nc<7, true>(p, batch, s, pdl);
       case 6: return launch_build_nc<6, true>(p, batch, s, pdl);
@@ -743,7 +754,12 @@ cudaError_t launch_build(const BuildParams& p0, int level_src, int batch, cudaSt
       default: return launch_build_nc<1, true>(p, batch, s, pdl);
     }
   }
-  switch (chunk_for(p.KL, 4)) {
+  static const int cap1 = [] {
+    const char* e = std::getenv("FLLF_BUILD_CHUNK");
+    const int v = e ? std::atoi(e) : 4;
+    return v >= 1 && v <= 4 ? v : 4;
+  }();
+  switch (chunk_for(p.KL, cap1)) {
     case 4: return launch_build_nc<4, false>(p, batch, s, pdl);
     case 3: return launch_build_nc<3, false>(p, batch, s, pdl);
     case 2: return launch_build_nc<2, false>(p, batch, s, pdl);
@@ -754,7 +770,13 @@ cudaError_t launch_build(const BuildParams& p0, int level_src, int batch, cudaSt
 template <bool L0, bool HD, bool MP>
 static cudaError_t launch_apply_t(const ApplyParams& p, int batch, cudaStream_t s, bool pdl) {
   dim3 grid((p.Wf + 119) / 120, (p.Hc + 3) / 4, batch);
-  const int smem = APPLY_STAGES * apply_stage_bytes<L0>();
+  const int smem = apply_stages<L0>() * apply_stage_bytes<L0>();
+  static bool attr_set = false;  // > 48 KB of dynamic shared memory needs an opt-in
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_apply<L0, HD, MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
   return launch_ex(k_apply<L0, HD, MP>, grid, dim3(160), smem, s, pdl, p);
 }
 
