@@ -142,7 +142,7 @@ __device__ __forceinline__ float hfilt_r(float a, float b) {
 // picks NC dividing the local order count) and NR real channels (1: G_l[I];
 // 2: the sigma / m maps).  EDGE = false: all 64 fine columns of the warp lie
 // inside the row, no index mapping; EDGE = true: reflect-101 per column.
-template <int NC, int NR, bool FROM_IMAGE, bool EDGE>
+template <int NC, int NR, bool FROM_IMAGE, bool EDGE, bool ZFIRST>
 struct BuildWarp {
   static constexpr int NCX = NC > 0 ? NC : 1;
   static constexpr int NCL = FROM_IMAGE ? 1 : NCX;  // complex values loaded per row
@@ -157,7 +157,8 @@ struct BuildWarp {
 
   const BuildParams& P;
   int o0, x, c0, rc0, rc1, g0;
-  bool store_lane, halo_l, halo_r, do_real;
+  bool store_lane, halo, do_real;
+  int hoff;  // offset (float2) from column x to this lane's halo column
   const float* rsrc[NR];
   float* rdst[NR];
   long long rpitch;
@@ -179,8 +180,10 @@ struct BuildWarp {
     do_real = (chunk == 0);
     // halo columns of the destination Z planes (see ZHALO): col -1 := x_1,
     // col Wc := x_{Wc-1} (Wf even) or x_{Wc-2} (Wf odd)
-    halo_l = store_lane && x == 1;
-    halo_r = store_lane && x == ((P.Wf & 1) ? P.Wc - 2 : P.Wc - 1);
+    const bool halo_l = store_lane && x == 1;
+    const bool halo_r = store_lane && x == ((P.Wf & 1) ? P.Wc - 2 : P.Wc - 1);
+    halo = halo_l || halo_r;
+    hoff = halo_l ? -1 - x : P.Wc - x;
     if (FROM_IMAGE) {
       rsrc[0] = P.img.p + frame * P.img.fstride;
       if (NR > 1) rsrc[NR - 1] = P.img2.p + frame * P.img2.fstride;
@@ -220,10 +223,10 @@ struct BuildWarp {
       d.r[i] = EDGE ? make_float2(__ldg(rp + rc0), __ldg(rp + rc1)) : ldg2(rp + c0);
     }
     if (!FROM_IMAGE && NC > 0) {
-      const float2* zp = zsrc + (long long)rr * P.src.zpitch;
+      const float2* q = zsrc + (long long)rr * P.src.zpitch;
+      const long long ks = P.src.kstride_z;
 #pragma unroll
-      for (int i = 0; i < NCX; ++i) {
-        const float2* q = zp + (long long)i * P.src.kstride_z;
+      for (int i = 0; i < NCX; ++i, q += ks) {
         if (EDGE) {
           d.c[i][0] = __ldg(q + rc0);
           d.c[i][1] = __ldg(q + rc1);
@@ -250,9 +253,8 @@ struct BuildWarp {
       const float2 ea = pfma(bc(W2), ea_, Pc[0]);
       const float2 eb = pfma(bc(W2), eb_, Pc[1]);
       const float2 h = hfilt_c(ea, eb);
-      if (store_lane) q[x] = h;
-      if (halo_l) q[-1] = h;
-      if (halo_r) q[P.Wc] = h;
+      if (store_lane) q[0] = h;
+      if (halo) q[hoff] = h;
     }
     if (!ONLY) {
       vstep(Pc[0], Ac[0], ea_, oa);
@@ -278,47 +280,52 @@ struct BuildWarp {
       }
     }
     if (NC == 0) return;
-    float2* zrow = zdst + (long long)emit * P.dst.zpitch;
+    // store pointer of channel 0 at (emit, x); channels advance by kstride
+    float2* q = zdst + ((long long)emit * P.dst.zpitch + x);
+    const long long ks = P.dst.kstride_z;
     if (FROM_IMAGE) {
       // e^{i k w_1 I} for the 4 pixels (even/odd row x col a/b), (s, c) layout
       float2 zc[4], zp[4];
       float tc[4];
       const float I4[4] = {d.e.r[0].x, d.e.r[0].y, d.o.r[0].x, d.o.r[0].y};
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int u = 0; u < 4; ++u) {
         float sn, cs;
-        sincos_turns(I4[q], P.invT, &sn, &cs);
+        sincos_turns(I4[u], P.invT, &sn, &cs);
         const float2 z1 = make_float2(sn, cs);
-        tc[q] = 2.f * cs;
-        if (g0 == 1) {
-          zp[q] = make_float2(0.f, 1.f);
-          zc[q] = z1;
+        tc[u] = 2.f * cs;
+        if (ZFIRST) {
+          zp[u] = make_float2(0.f, 1.f);
+          zc[u] = z1;
         } else {
           // chunk start: e^{i g0 theta} directly (range-reduced in turns),
           // e^{i (g0-1) theta} = e^{i g0 theta} e^{-i theta}
           float sg, cg;
-          sincos_turns_n(I4[q], P.invT, g0, &sg, &cg);
-          zc[q] = make_float2(sg, cg);
-          zp[q] = make_float2(fmaf(sg, cs, -cg * sn), fmaf(cg, cs, sg * sn));
+          sincos_turns_n(I4[u], P.invT, g0, &sg, &cg);
+          zc[u] = make_float2(sg, cg);
+          zp[u] = make_float2(fmaf(sg, cs, -cg * sn), fmaf(cg, cs, sg * sn));
         }
       }
 #pragma unroll
       for (int i = 0; i < NCX; ++i) {
-        chan<EMIT, ONLY>(Pc[i], Ac[i], zc[0], zc[1], zc[2], zc[3], zrow + (long long)i * P.dst.kstride_z);
+        chan<EMIT, ONLY>(Pc[i], Ac[i], zc[0], zc[1], zc[2], zc[3], q);
+        q += ks;
         if (i + 1 < NCX) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float2 zn = pfma(bc(-1.f), zp[q], pmul(bc(tc[q]), zc[q]));
-            zp[q] = zc[q];
-            zc[q] = zn;
+          for (int u = 0; u < 4; ++u) {
+            const float2 zn = pfma(bc(-1.f), zp[u], pmul(bc(tc[u]), zc[u]));
+            zp[u] = zc[u];
+            zc[u] = zn;
           }
         }
       }
     } else {
 #pragma unroll
       for (int i = 0; i < NCX; ++i)
-        chan<EMIT, ONLY>(Pc[i], Ac[i], d.e.c[i][0], d.e.c[i][1], d.o.c[i][0], d.o.c[i][1],
-                         zrow + (long long)i * P.dst.kstride_z);
+      {
+        chan<EMIT, ONLY>(Pc[i], Ac[i], d.e.c[i][0], d.e.c[i][1], d.o.c[i][0], d.o.c[i][1], q);
+        q += ks;
+      }
     }
   }
 
@@ -364,12 +371,24 @@ __global__ void __launch_bounds__(32) k_build(const BuildParams P) {
   if (FROM_IMAGE)
     interior = interior && ((reinterpret_cast<uintptr_t>(P.img.p) & 7) == 0) && ((P.img.pitch & 1) == 0) &&
                (NR < 2 || (((reinterpret_cast<uintptr_t>(P.img2.p) & 7) == 0) && P.img2.pitch == P.img.pitch));
+  // chunks starting at order 1 need no chunk-start phasor (level 0 only)
+  const bool zfirst = !FROM_IMAGE || (P.kbase + chunk * NC == 1);
   if (interior) {
-    BuildWarp<NC, NR, FROM_IMAGE, false> w(P, cb, o0, chunk, frame);
-    w.run(R);
+    if (zfirst) {
+      BuildWarp<NC, NR, FROM_IMAGE, false, true> w(P, cb, o0, chunk, frame);
+      w.run(R);
+    } else {
+      BuildWarp<NC, NR, FROM_IMAGE, false, false> w(P, cb, o0, chunk, frame);
+      w.run(R);
+    }
   } else {
-    BuildWarp<NC, NR, FROM_IMAGE, true> w(P, cb, o0, chunk, frame);
-    w.run(R);
+    if (zfirst) {
+      BuildWarp<NC, NR, FROM_IMAGE, true, true> w(P, cb, o0, chunk, frame);
+      w.run(R);
+    } else {
+      BuildWarp<NC, NR, FROM_IMAGE, true, false> w(P, cb, o0, chunk, frame);
+      w.run(R);
+    }
   }
 }
 
@@ -740,8 +759,8 @@ cudaError_t launch_build(const BuildParams& p0, int level_src, int batch, cudaSt
   if (level_src == 0) {
     static const int cap0 = [] {
       const char* e = std::getenv("FLLF_BUILD0_CHUNK");
-      const int v = e ? std::atoi(e) : 8;
-      return v >= 1 && v <= 8 ? v : 8;
+      const int v = e ? std::atoi(e) : 4;  // measured best on B200
+      return v >= 1 && v <= 8 ? v : 4;
     }();
     switch (chunk_for(p.KL, cap0)) {
       case 8: return launch_build_nc<8, true>(p, batch, s, pdl);
@@ -756,8 +775,8 @@ cudaError_t launch_build(const BuildParams& p0, int level_src, int batch, cudaSt
   }
   static const int cap1 = [] {
     const char* e = std::getenv("FLLF_BUILD_CHUNK");
-    const int v = e ? std::atoi(e) : 4;
-    return v >= 1 && v <= 4 ? v : 4;
+    const int v = e ? std::atoi(e) : 2;  // measured best on B200
+    return v >= 1 && v <= 4 ? v : 2;
   }();
   switch (chunk_for(p.KL, cap1)) {
     case 4: return launch_build_nc<4, false>(p, batch, s, pdl);
