@@ -147,6 +147,14 @@ FLLF_API fllf_status fllf_filter_host(fllf_plan p, const float* h_img, float* h_
 FLLF_API fllf_status fllf_coefficients(int K, double T, double sigma_r, double m, double* omega_out,
                               double* a_out);
 
+/* Host helper, Eq. 12: the period T minimising
+ *   E_K(T) = erfc(pi sigma_r (2K+1) / T) + erfc((T - R) / sigma_r)
+ * over T in [R, R + 12 sigma_r] (dense grid + golden-section refinement to
+ * 1e-6); R is the number of tones (256 for 8-bit).  Reading R11: the
+ * paper's sigma is sigma_r.  sigma_r = 30, K = 10 gives 405.5 (paper: 405.9,
+ * P:296). */
+FLLF_API fllf_status fllf_optimal_period(int K, double sigma_r, double R, double* T_out);
+
 /* Introspection (tests, tooling). */
 FLLF_API fllf_status fllf_plan_level_dims(fllf_plan p, int level, int* H, int* W);
 FLLF_API fllf_status fllf_workspace_bytes(fllf_plan p, size_t* bytes);

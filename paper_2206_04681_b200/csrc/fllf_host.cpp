@@ -152,6 +152,43 @@ fllf_status fllf_coefficients(int K, double T, double sigma_r, double m, double*
   return FLLF_OK;
 }
 
+static double period_error(double T, int K, double sigma, double R) {
+  return std::erfc(kPi * sigma * (2.0 * K + 1.0) / T) + std::erfc((T - R) / sigma);
+}
+
+fllf_status fllf_optimal_period(int K, double sigma_r, double R, double* T_out) {
+  if (!T_out) return fail(FLLF_ERR_BAD_POINTER, "fllf_optimal_period: NULL output");
+  if (K < 1 || !(sigma_r > 0) || !is_finite(sigma_r) || !(R > 0) || !is_finite(R))
+    return fail(FLLF_ERR_INVALID_ARGUMENT, "fllf_optimal_period: need K>=1, sigma_r>0, R>0");
+  const double lo = R, hi = R + 12.0 * sigma_r;
+  const int n = 4000;
+  int best = 0;
+  double bv = period_error(lo, K, sigma_r, R);
+  for (int i = 1; i <= n; ++i) {
+    const double v = period_error(lo + (hi - lo) * i / n, K, sigma_r, R);
+    if (v < bv) {
+      bv = v;
+      best = i;
+    }
+  }
+  double a = lo + (hi - lo) * std::max(best - 1, 0) / n, b = lo + (hi - lo) * std::min(best + 1, n) / n;
+  const double phi = (std::sqrt(5.0) - 1.0) / 2.0;
+  double c = b - phi * (b - a), d = a + phi * (b - a);
+  while (b - a > 1e-6) {
+    if (period_error(c, K, sigma_r, R) < period_error(d, K, sigma_r, R)) {
+      b = d;
+      d = c;
+      c = b - phi * (b - a);
+    } else {
+      a = c;
+      c = d;
+      d = a + phi * (b - a);
+    }
+  }
+  *T_out = 0.5 * (a + b);
+  return FLLF_OK;
+}
+
 fllf_status fllf_plan_create(int H, int W, int levels, int K, double T, double sigma_r, double m,
                              fllf_plan* out) {
   fllf_plan_desc d{};

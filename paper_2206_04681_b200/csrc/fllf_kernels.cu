@@ -39,6 +39,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <cstdlib>
+#include <algorithm>
 
 #include "fllf_internal.h"
 #include "fllf_ptx.h"
@@ -157,8 +158,8 @@ struct BuildWarp {
 
   const BuildParams& P;
   int o0, x, c0, rc0, rc1, g0;
-  bool store_lane, halo, do_real;
-  int hoff;  // offset (float2) from column x to this lane's halo column
+  bool store_lane, halo_l, halo_r, do_real;
+  int hoff_r;  // offset (float2) from column x to the right halo column Wc
   const float* rsrc[NR];
   float* rdst[NR];
   long long rpitch;
@@ -180,10 +181,10 @@ struct BuildWarp {
     do_real = (chunk == 0);
     // halo columns of the destination Z planes (see ZHALO): col -1 := x_1,
     // col Wc := x_{Wc-1} (Wf even) or x_{Wc-2} (Wf odd)
-    const bool halo_l = store_lane && x == 1;
-    const bool halo_r = store_lane && x == ((P.Wf & 1) ? P.Wc - 2 : P.Wc - 1);
-    halo = halo_l || halo_r;
-    hoff = halo_l ? -1 - x : P.Wc - x;
+    // (both can hold for one lane when Wc = 3)
+    halo_l = store_lane && x == 1;
+    halo_r = store_lane && x == ((P.Wf & 1) ? P.Wc - 2 : P.Wc - 1);
+    hoff_r = P.Wc - x;
     if (FROM_IMAGE) {
       rsrc[0] = P.img.p + frame * P.img.fstride;
       if (NR > 1) rsrc[NR - 1] = P.img2.p + frame * P.img2.fstride;
@@ -254,7 +255,8 @@ struct BuildWarp {
       const float2 eb = pfma(bc(W2), eb_, Pc[1]);
       const float2 h = hfilt_c(ea, eb);
       if (store_lane) q[0] = h;
-      if (halo) q[hoff] = h;
+      if (halo_l) q[-2] = h;  // x == 1: column -1
+      if (halo_r) q[hoff_r] = h;
     }
     if (!ONLY) {
       vstep(Pc[0], Ac[0], ea_, oa);
@@ -329,32 +331,52 @@ struct BuildWarp {
     }
   }
 
+  // Stream the strip: pairs 0 (halo rows) .. R (last output pairs) and the
+  // final row (even row of pair R+1), keeping PD row pairs in flight.  Pair p
+  // lives in buf[p % PD] and uses roles (S1, S0) for even p, (S0, S1) for odd
+  // p; PD is even so both are compile-time inside the unrolled bodies.
+  template <int PD>
   __device__ __forceinline__ void run(int R) {
-    Pair BA, BB;
-    load_pair(0, BA);
-    load_pair(1, BB);
-    proc<false, false>(BA, S1c, S0c, S1r, S0r, 0);  // p = 0: halo rows
-    load_pair(2, BA);
-    proc<false, false>(BB, S0c, S1c, S0r, S1r, 0);  // p = 1: first pair, nothing to emit
-    load_pair(3, BB);
+    static_assert(PD % 2 == 0 && PD >= 2, "PD must be even");
+    Pair buf[PD];
+#pragma unroll
+    for (int i = 0; i < PD; ++i) load_pair(i, buf[i]);
+    proc<false, false>(buf[0], S1c, S0c, S1r, S0r, 0);  // p = 0: halo rows
+    load_pair(PD, buf[0]);
+    proc<false, false>(buf[1], S0c, S1c, S0r, S1r, 0);  // p = 1: first pair, nothing to emit
+    load_pair(PD + 1, buf[1]);
     int p = 2;
 #pragma unroll 1
-    for (; p + 1 <= R; p += 2) {
-      proc<true, false>(BA, S1c, S0c, S1r, S0r, o0 + p - 2);
-      load_pair(p + 2, BA);
-      proc<true, false>(BB, S0c, S1c, S0r, S1r, o0 + p - 1);
-      load_pair(p + 3, BB);
+    for (; p + PD - 1 <= R; p += PD) {
+#pragma unroll
+      for (int i = 0; i < PD; ++i) {
+        if ((i & 1) == 0)
+          proc<true, false>(buf[(2 + i) % PD], S1c, S0c, S1r, S0r, o0 + p + i - 2);
+        else
+          proc<true, false>(buf[(2 + i) % PD], S0c, S1c, S0r, S1r, o0 + p + i - 2);
+        load_pair(p + i + PD, buf[(2 + i) % PD]);
+      }
     }
-    if (p <= R) {
-      proc<true, false>(BA, S1c, S0c, S1r, S0r, o0 + p - 2);
-      proc<true, true>(BB, S0c, S1c, S0r, S1r, o0 + R - 1);  // final row = even row of pair R+1
-    } else {
-      proc<true, true>(BA, S1c, S0c, S1r, S0r, o0 + R - 1);
+    // fewer than PD pairs left, then the final row (pair R+1)
+#pragma unroll
+    for (int i = 0; i < PD; ++i) {
+      const int pp = p + i;
+      if (pp <= R) {
+        if ((i & 1) == 0)
+          proc<true, false>(buf[(2 + i) % PD], S1c, S0c, S1r, S0r, o0 + pp - 2);
+        else
+          proc<true, false>(buf[(2 + i) % PD], S0c, S1c, S0r, S1r, o0 + pp - 2);
+      } else if (pp == R + 1) {
+        if ((i & 1) == 0)
+          proc<true, true>(buf[(2 + i) % PD], S1c, S0c, S1r, S0r, o0 + R - 1);
+        else
+          proc<true, true>(buf[(2 + i) % PD], S0c, S1c, S0r, S1r, o0 + R - 1);
+      }
     }
   }
 };
 
-template <int NC, int NR, bool FROM_IMAGE>
+template <int NC, int NR, bool FROM_IMAGE, bool SMALL>
 __global__ void __launch_bounds__(32) k_build(const BuildParams P) {
   pdl_wait();     // the previous level's planes are complete
   pdl_trigger();  // let the next kernel get scheduled
@@ -376,18 +398,18 @@ __global__ void __launch_bounds__(32) k_build(const BuildParams P) {
   if (interior) {
     if (zfirst) {
       BuildWarp<NC, NR, FROM_IMAGE, false, true> w(P, cb, o0, chunk, frame);
-      w.run(R);
+      w.template run<(FROM_IMAGE || SMALL) ? 4 : 2>(R);
     } else {
       BuildWarp<NC, NR, FROM_IMAGE, false, false> w(P, cb, o0, chunk, frame);
-      w.run(R);
+      w.template run<(FROM_IMAGE || SMALL) ? 4 : 2>(R);
     }
   } else {
     if (zfirst) {
       BuildWarp<NC, NR, FROM_IMAGE, true, true> w(P, cb, o0, chunk, frame);
-      w.run(R);
+      w.template run<(FROM_IMAGE || SMALL) ? 4 : 2>(R);
     } else {
       BuildWarp<NC, NR, FROM_IMAGE, true, false> w(P, cb, o0, chunk, frame);
-      w.run(R);
+      w.template run<(FROM_IMAGE || SMALL) ? 4 : 2>(R);
     }
   }
 }
@@ -407,10 +429,26 @@ __host__ __device__ constexpr int apply_stage_bytes() {
   return 6 * CROW_BYTES + (LEVEL0 ? 0 : 8 * FROW_BYTES);
 }
 
-// Warp-specialised: warps 0..3 compute (one coarse row each), warp 4 is the
-// TMA producer that refills a stage as soon as the 4 consumer warps released it.
+// Persistent, warp-specialised: a CTA loops over tiles (4 coarse rows x 30
+// coarse column pairs of one frame); warps 0..3 compute (one coarse row each),
+// warp 4 is the TMA producer that streams (tile, order) stages through the
+// shared-memory ring ahead of the consumers -- across tile boundaries, so the
+// start-up latency of a tile is hidden behind the previous one.
+struct ApplyTile {
+  int jb, r0, frame;
+};
+__device__ __forceinline__ ApplyTile apply_tile(int t, const ApplyParams& P) {
+  const int nx = (P.Wf + 119) / 120, ny = (P.Hc + 3) / 4;
+  ApplyTile T;
+  T.jb = t % nx;
+  t /= nx;
+  T.r0 = (t % ny) * 4;
+  T.frame = t / ny;
+  return T;
+}
+
 template <bool LEVEL0, bool HAS_D, bool MAPS>
-__global__ void __launch_bounds__(160, MAPS ? 2 : 3) k_apply(const ApplyParams P) {
+__global__ void __launch_bounds__(160, MAPS ? 2 : 3) k_apply(const ApplyParams P, const int ntiles) {
   constexpr int S = apply_stages<LEVEL0>();
   constexpr int STAGE = apply_stage_bytes<LEVEL0>();
   constexpr int FOFF = 6 * CROW_BYTES;
@@ -420,26 +458,14 @@ __global__ void __launch_bounds__(160, MAPS ? 2 : 3) k_apply(const ApplyParams P
 
   // PDL: the Z / G planes of the build pass are complete once the first apply
   // of the sequence has waited; only D_{l+1} (previous apply) needs a wait,
-  // taken right before it is read after the order loop.
+  // taken right before it is first read.
   if (P.wait_first) pdl_wait();
   pdl_trigger();
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
-  const int jb = blockIdx.x;         // fine columns [120 jb, 120 jb + 120)
-  const int r0 = blockIdx.y * 4;     // coarse rows r0 .. r0+3, one per warp
-  const int frame = blockIdx.z;
-  const int r = r0 + warp;
-  const int j = jb * 30 + lane - 1;  // coarse columns 2j, 2j+1 -> fine columns 4j..4j+3
-  const bool rowok = r < P.Hc;
-  const bool act = rowok && lane >= 1 && lane <= 30 && 4 * j < P.Wf;
   const int KL = P.KL;
 
-  // ---- TMA producer (thread 0): per order k, 6 coarse row segments of
-  // Z_{l+1,k} (coarse cols 2j0 .. 2j0+63, j0 = 30 jb - 1) and, for l >= 1,
-  // 8 fine row segments of Z_{l,k} (fine cols 4j0 .. 4j0+127)
-  const float2* zc0 = P.coarse.Z + frame * P.coarse.fstride_z + (60 * jb - 2);
-  const float2* zf0 = LEVEL0 ? nullptr : P.fine.Z + frame * P.fine.fstride_z + (120 * jb - 4);
   if (tid == 0) {
 #pragma unroll
     for (int s = 0; s < S; ++s) {
@@ -449,26 +475,35 @@ __global__ void __launch_bounds__(160, MAPS ? 2 : 3) k_apply(const ApplyParams P
     fence_mbar_init();
   }
   __syncthreads();
+
   if (warp == 4) {
-    // ---- producer warp: one elected lane issues all bulk copies
+    // ---- producer: one lane issues, per (tile, order k), 6 coarse row
+    // segments of Z_{l+1,k} (coarse cols 2j0 .. 2j0+63, j0 = 30 jb - 1) and,
+    // for l >= 1, 8 fine row segments of Z_{l,k} (fine cols 4j0 .. 4j0+127)
     if (lane == 0) {
-      for (int k = 0; k < KL; ++k) {
-        const int s = k % S;
-        if (k >= S) mbar_wait_parity(&empty[s], ((k / S) - 1) & 1);
-        unsigned char* st = smem + s * STAGE;
-        mbar_arrive_expect_tx(&full[s], STAGE);
-        const float2* zc = zc0 + (long long)k * P.coarse.kstride_z;
+      int it = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const ApplyTile T = apply_tile(t, P);
+        const float2* zc0 = P.coarse.Z + T.frame * P.coarse.fstride_z + (60 * T.jb - 2);
+        const float2* zf0 = LEVEL0 ? nullptr : P.fine.Z + T.frame * P.fine.fstride_z + (120 * T.jb - 4);
+        for (int k = 0; k < KL; ++k, ++it) {
+          const int s = it % S;
+          if (it >= S) mbar_wait_parity(&empty[s], ((it / S) - 1) & 1);
+          unsigned char* st = smem + s * STAGE;
+          mbar_arrive_expect_tx(&full[s], STAGE);
+          const float2* zc = zc0 + (long long)k * P.coarse.kstride_z;
 #pragma unroll
-        for (int t = 0; t < 6; ++t) {
-          const int cr = upmap(r0 - 1 + t, P.Hc, P.Hf);
-          tma_load_1d(st + t * CROW_BYTES, zc + (long long)cr * P.coarse.zpitch, CROW_BYTES, &full[s]);
-        }
-        if (!LEVEL0) {
-          const float2* zf = zf0 + (long long)k * P.fine.kstride_z;
+          for (int q = 0; q < 6; ++q) {
+            const int cr = upmap(T.r0 - 1 + q, P.Hc, P.Hf);
+            tma_load_1d(st + q * CROW_BYTES, zc + (long long)cr * P.coarse.zpitch, CROW_BYTES, &full[s]);
+          }
+          if (!LEVEL0) {
+            const float2* zf = zf0 + (long long)k * P.fine.kstride_z;
 #pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            const int fr = min(2 * r0 + t, P.Hf - 1);
-            tma_load_1d(st + FOFF + t * FROW_BYTES, zf + (long long)fr * P.fine.zpitch, FROW_BYTES, &full[s]);
+            for (int q = 0; q < 8; ++q) {
+              const int fr = min(2 * T.r0 + q, P.Hf - 1);
+              tma_load_1d(st + FOFF + q * FROW_BYTES, zf + (long long)fr * P.fine.zpitch, FROW_BYTES, &full[s]);
+            }
           }
         }
       }
@@ -476,174 +511,47 @@ __global__ void __launch_bounds__(160, MAPS ? 2 : 3) k_apply(const ApplyParams P
     return;
   }
 
-  // ---- per-thread setup (overlaps the first copies)
-  const bool row1 = 2 * r + 1 < P.Hf;
-  const int yf[2] = {min(2 * r, P.Hf - 1), min(row1 ? 2 * r + 1 : 2 * r, P.Hf - 1)};
-  const int xf0 = 4 * j;
-  const bool fvec_ok = xf0 >= 0 && xf0 + 3 < P.Wf;
-  int xf[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) xf[q] = min(max(xf0 + q, 0), P.Wf - 1);
-  const int cr[3] = {upmap(r - 1, P.Hc, P.Hf), min(r, P.Hc - 1), upmap(r + 1, P.Hc, P.Hf)};
-  const bool cvec = (2 * j >= 0) && (2 * j + 1 < P.Wc);
-  const int cc0 = upmap(2 * j, P.Wc, P.Wf), cc1 = upmap(2 * j + 1, P.Wc, P.Wf);
-
-  float g[8];
-  {
+  // ---- consumers
+  const bool img_al = ((reinterpret_cast<uintptr_t>(P.img.p) & 15) == 0) && ((P.img.pitch & 3) == 0);
+  const bool out_al = ((reinterpret_cast<uintptr_t>(P.out) & 15) == 0) && ((P.out_pitch & 3) == 0);
+  // g = I (level 0) or G_l at the thread's 2x4 fine pixels of tile T
+  auto load_g = [&](const ApplyTile& T, float (&g)[8]) {
+    const int r = min(T.r0 + warp, P.Hc - 1);
+    const int j = T.jb * 30 + lane - 1;
+    const int xf0 = 4 * j;
+    const bool fvec_ok = xf0 >= 0 && xf0 + 3 < P.Wf;
     const float* base;
     long long pitch;
     bool al;
     if (LEVEL0) {
-      base = P.img.p + frame * P.img.fstride;
+      base = P.img.p + T.frame * P.img.fstride;
       pitch = P.img.pitch;
-      al = ((reinterpret_cast<uintptr_t>(P.img.p) & 15) == 0) && ((P.img.pitch & 3) == 0);
+      al = img_al;
     } else {
-      base = P.fine.G + frame * P.fine.fstride_r;
+      base = P.fine.G + T.frame * P.fine.fstride_r;
       pitch = P.fine.pitch;
       al = true;
     }
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
-      const float* rp = base + (long long)yf[t] * pitch;
+      const float* rp = base + (long long)min(2 * r + t, P.Hf - 1) * pitch;
       if (fvec_ok && al) {
         const float4 v = ldg4(rp + xf0);
         g[4 * t + 0] = v.x; g[4 * t + 1] = v.y; g[4 * t + 2] = v.z; g[4 * t + 3] = v.w;
       } else {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) g[4 * t + q] = __ldg(rp + xf[q]);
+        for (int q = 0; q < 4; ++q) g[4 * t + q] = __ldg(rp + min(max(xf0 + q, 0), P.Wf - 1));
       }
     }
-  }
-  float mA[8], mR[8], mQ[8];
-  if (MAPS) {
-    const float* sptr;
-    const float* mptr;
-    long long mp;
-    if (LEVEL0) {
-      sptr = P.smap.p; mptr = P.mmap.p; mp = P.smap.pitch;
-    } else {
-      sptr = P.fine.MS; mptr = P.fine.MM; mp = P.fine.pitch;
-    }
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const long long off = (long long)yf[t] * mp + xf[q];
-        const float sg = __ldg(sptr + off), m = __ldg(mptr + off);
-        const float beta = P.hq * sg * sg;
-        const int p = 4 * t + q;
-        const float kb = (float)P.kbase;
-        // a_k = m sigma^3 c0 k exp(-k^2 beta), carried with R = exp(-(2k+1) beta), Q = exp(-2 beta)
-        mA[p] = m * sg * sg * sg * P.c0 * kb * __expf(-kb * kb * beta);
-        mR[p] = __expf(-(2.f * kb + 1.f) * beta);
-        mQ[p] = __expf(-2.f * beta);
-      }
-    }
-  }
-  // Chebyshev state per pixel, (c, s) layout: z = e^{i k w_1 g}, zp = e^{i (k-1) w_1 g}
-  float2 z[8], zp[8], acc[8];
-  float tc[8];
-  const int g0 = P.kbase;
-#pragma unroll
-  for (int p = 0; p < 8; ++p) {
-    float sn, cs;
-    sincos_turns(g[p], P.invT, &sn, &cs);
-    const float2 z1 = make_float2(cs, sn);
-    tc[p] = 2.f * cs;
-    if (g0 == 1) {
-      zp[p] = make_float2(1.f, 0.f);
-      z[p] = z1;
-    } else {
-      float sg, cg;
-      sincos_turns_n(g[p], P.invT, g0, &sg, &cg);
-      z[p] = make_float2(cg, sg);
-      zp[p] = make_float2(fmaf(cg, cs, sg * sn), fmaf(sg, cs, -cg * sn));
-    }
-    acc[p] = make_float2(0.f, 0.f);
-  }
-
-  // ---- order loop (unrolled by 2 so the recurrence state rotates without moves)
-#pragma unroll 2
-  for (int k = 0; k < KL; ++k) {
-    const int s = k % S;
-    mbar_wait_parity(&full[s], (k / S) & 1);
-    const unsigned char* st = smem + s * STAGE;
-    float2 h[3][4];
-#pragma unroll
-    for (int t = 0; t < 3; ++t) {
-      const float4 qv = *reinterpret_cast<const float4*>(st + (warp + t) * CROW_BYTES + lane * 16);
-      const float2 x0 = lo2(qv), x1 = hi2(qv);
-      const float2 L = shfl_up2(x1), Rn = shfl_down2(x0);
-      // horizontal polyphase (unscaled): even fine col x_{c-1} + 6 x_c + x_{c+1} (/8), odd x_c + x_{c+1} (/2)
-      h[t][0] = pfma(bc(6.f), x0, padd(L, x1));
-      h[t][1] = padd(x0, x1);
-      h[t][2] = pfma(bc(6.f), x1, padd(x0, Rn));
-      h[t][3] = padd(x1, Rn);
-    }
-    float4 fz[4];
-    if (!LEVEL0) {
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        const unsigned char* fr = st + FOFF + (2 * warp + t) * FROW_BYTES + lane * 32;
-        fz[2 * t] = *reinterpret_cast<const float4*>(fr);
-        fz[2 * t + 1] = *reinterpret_cast<const float4*>(fr + 16);
-      }
-    }
-    float2 waa, w1, w2, w3;
-    if (MAPS) {
-      waa = bc(1.f); w1 = bc(-1.f / 64.f); w2 = bc(-1.f / 16.f); w3 = bc(-1.f / 4.f);
-    } else {
-      waa = P.wk[k][0]; w1 = P.wk[k][1]; w2 = P.wk[k][2]; w3 = P.wk[k][3];
-    }
-    const float kk = (float)(P.kbase + k);
-    const float kratio = (kk + 1.f) / kk;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      // vertical: even fine row (h[-1] + 6 h[0] + h[+1]) (/8); odd (h[0] + h[+1]) (/2)
-      const float2 re = pfma(bc(6.f), h[1][q], padd(h[0][q], h[2][q]));
-      const float2 ro = padd(h[1][q], h[2][q]);
-      const float2 we = (q & 1) ? w2 : w1;  // even row: ee 1/64, eo 1/16
-      const float2 wo = (q & 1) ? w3 : w2;  // odd row:  oe 1/16, oo 1/4
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        const int p = 4 * t + q;
-        const float2 raw = t == 0 ? re : ro;
-        const float2 w = t == 0 ? we : wo;
-        float2 V;  // (Im, Re) of a_k (Z_l - up Z_{l+1}) at this pixel
-        float2 zf = make_float2(0.f, 0.f);
-        if (!LEVEL0) {
-          const float4 fv = fz[2 * t + (q >> 1)];
-          zf = (q & 1) ? hi2(fv) : lo2(fv);
-        }
-        if (MAPS) {
-          V = pmul(bc(mA[p]), LEVEL0 ? pmul(w, raw) : pfma(w, raw, zf));
-        } else {
-          V = LEVEL0 ? pmul(w, raw) : pfma(w, raw, pmul(waa, zf));
-        }
-        // acc += (c V.im, s V.re); result = acc.x - acc.y = a_k Im(e^{-i k w_1 g} (...))
-        acc[p] = pfma(z[p], V, acc[p]);
-        const float2 zn = pfma(bc(-1.f), zp[p], pmul(bc(tc[p]), z[p]));
-        zp[p] = z[p];
-        z[p] = zn;
-        if (MAPS) {
-          mA[p] *= mR[p] * kratio;
-          mR[p] *= mQ[p];
-        }
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with slot s
-  }
-
-  float res[8];
-#pragma unroll
-  for (int p = 0; p < 8; ++p) res[p] = acc[p].x - acc[p].y;
-
-  // --- collapse: + up(D_{l+1}) (written by the previous apply grid)
-  if (HAS_D) {
-    pdl_wait();
-    float dq[3][2];
-    const float* dc = P.coarse.D + frame * P.coarse.fstride_r;
+  };
+  // coarse D_{l+1} at rows r-1..r+1, columns 2j, 2j+1 (polyphase border rule)
+  auto load_d = [&](const ApplyTile& T, float (&dq)[3][2]) {
+    const int r = T.r0 + warp;
+    const int j = T.jb * 30 + lane - 1;
+    const int cr[3] = {upmap(r - 1, P.Hc, P.Hf), min(r, P.Hc - 1), upmap(r + 1, P.Hc, P.Hf)};
+    const bool cvec = (2 * j >= 0) && (2 * j + 1 < P.Wc);
+    const int cc0 = upmap(2 * j, P.Wc, P.Wf), cc1 = upmap(2 * j + 1, P.Wc, P.Wf);
+    const float* dc = P.coarse.D + T.frame * P.coarse.fstride_r;
 #pragma unroll
     for (int t = 0; t < 3; ++t) {
       const float* rp = dc + (long long)cr[t] * P.coarse.pitch;
@@ -656,57 +564,214 @@ __global__ void __launch_bounds__(160, MAPS ? 2 : 3) k_apply(const ApplyParams P
         dq[t][1] = __ldg(rp + cc1);
       }
     }
-    float hd[3][4];
-#pragma unroll
-    for (int t = 0; t < 3; ++t) {
-      const float x0 = dq[t][0], x1 = dq[t][1];
-      const float L = __shfl_up_sync(FULL, x1, 1);
-      const float Rn = __shfl_down_sync(FULL, x0, 1);
-      hd[t][0] = fmaf(6.f, x0, L + x1) * 0.125f;
-      hd[t][1] = (x0 + x1) * 0.5f;
-      hd[t][2] = fmaf(6.f, x1, x0 + Rn) * 0.125f;
-      hd[t][3] = (x1 + Rn) * 0.5f;
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      res[q] += 0.125f * fmaf(6.f, hd[1][q], hd[0][q] + hd[2][q]);
-      res[4 + q] += 0.5f * (hd[1][q] + hd[2][q]);
-    }
-  }
-  if (LEVEL0 && P.include_base) {
-#pragma unroll
-    for (int p = 0; p < 8; ++p) res[p] += g[p];
-  }
+  };
 
-  if (!act) return;
-  float* op;
-  long long opitch;
-  bool oal;
-  if (LEVEL0) {
-    op = P.out + frame * P.out_fstride;
-    opitch = P.out_pitch;
-    oal = ((reinterpret_cast<uintptr_t>(P.out) & 15) == 0) && ((P.out_pitch & 3) == 0);
-  } else {
-    op = P.fine.D + frame * P.fine.fstride_r;
-    opitch = P.fine.pitch;
-    oal = true;
-  }
+  bool waited = P.wait_first != 0;  // D_{l+1} is readable once the PDL wait returned
+  int it = 0;
+  float gnext[8];
+  if ((int)blockIdx.x < ntiles) load_g(apply_tile(blockIdx.x, P), gnext);
+#pragma unroll 1
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const ApplyTile T = apply_tile(t, P);
+    const int r = T.r0 + warp;
+    const int j = T.jb * 30 + lane - 1;  // coarse columns 2j, 2j+1 -> fine columns 4j..4j+3
+    const bool act = r < P.Hc && lane >= 1 && lane <= 30 && 4 * j < P.Wf;
+    float g[8];
 #pragma unroll
-  for (int t = 0; t < 2; ++t) {
-    if (t == 1 && !row1) break;
-    float* rp = op + (long long)(2 * r + t) * opitch;
-    if (fvec_ok && oal) {
-      *reinterpret_cast<float4*>(rp + xf0) = make_float4(res[4 * t], res[4 * t + 1], res[4 * t + 2], res[4 * t + 3]);
-    } else {
+    for (int p = 0; p < 8; ++p) g[p] = gnext[p];
+    if (t + (int)gridDim.x < ntiles) load_g(apply_tile(t + gridDim.x, P), gnext);  // next tile, early
+    float dq[3][2];
+    if (HAS_D && waited) load_d(T, dq);
+
+    float mA[8], mR[8], mQ[8];
+    if (MAPS) {
+      const float* sptr;
+      const float* mptr;
+      long long mp;
+      if (LEVEL0) {
+        sptr = P.smap.p; mptr = P.mmap.p; mp = P.smap.pitch;
+      } else {
+        sptr = P.fine.MS; mptr = P.fine.MM; mp = P.fine.pitch;
+      }
+      const int xf0 = 4 * j;
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (xf0 + q < P.Wf) rp[xf0 + q] = res[4 * t + q];
+      for (int tt = 0; tt < 2; ++tt) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const long long off = (long long)min(2 * r + tt, P.Hf - 1) * mp + min(max(xf0 + q, 0), P.Wf - 1);
+          const float sg = __ldg(sptr + off), m = __ldg(mptr + off);
+          const float beta = P.hq * sg * sg;
+          const int p = 4 * tt + q;
+          const float kb = (float)P.kbase;
+          // a_k = m sigma^3 c0 k exp(-k^2 beta), carried with R = exp(-(2k+1) beta), Q = exp(-2 beta)
+          mA[p] = m * sg * sg * sg * P.c0 * kb * __expf(-kb * kb * beta);
+          mR[p] = __expf(-(2.f * kb + 1.f) * beta);
+          mQ[p] = __expf(-2.f * beta);
+        }
+      }
+    }
+    // Chebyshev state per pixel, (c, s) layout: z = e^{i k w_1 g}, zp = e^{i (k-1) w_1 g}
+    float2 z[8], zp[8], acc[8];
+    float tc[8];
+    const int g0 = P.kbase;
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      float sn, cs;
+      sincos_turns(g[p], P.invT, &sn, &cs);
+      const float2 z1 = make_float2(cs, sn);
+      tc[p] = 2.f * cs;
+      if (g0 == 1) {
+        zp[p] = make_float2(1.f, 0.f);
+        z[p] = z1;
+      } else {
+        float sg, cg;
+        sincos_turns_n(g[p], P.invT, g0, &sg, &cg);
+        z[p] = make_float2(cg, sg);
+        zp[p] = make_float2(fmaf(cg, cs, sg * sn), fmaf(sg, cs, -cg * sn));
+      }
+      acc[p] = make_float2(0.f, 0.f);
+    }
+
+    // ---- order loop (unrolled by 2 so the recurrence state rotates without moves)
+#pragma unroll 2
+    for (int k = 0; k < KL; ++k, ++it) {
+      const int s = it % S;
+      mbar_wait_parity(&full[s], (it / S) & 1);
+      const unsigned char* st = smem + s * STAGE;
+      float2 h[3][4];
+#pragma unroll
+      for (int tt = 0; tt < 3; ++tt) {
+        const float4 qv = *reinterpret_cast<const float4*>(st + (warp + tt) * CROW_BYTES + lane * 16);
+        const float2 x0 = lo2(qv), x1 = hi2(qv);
+        const float2 L = shfl_up2(x1), Rn = shfl_down2(x0);
+        // horizontal polyphase (unscaled): even fine col x_{c-1} + 6 x_c + x_{c+1} (/8), odd x_c + x_{c+1} (/2)
+        h[tt][0] = pfma(bc(6.f), x0, padd(L, x1));
+        h[tt][1] = padd(x0, x1);
+        h[tt][2] = pfma(bc(6.f), x1, padd(x0, Rn));
+        h[tt][3] = padd(x1, Rn);
+      }
+      float4 fz[4];
+      if (!LEVEL0) {
+#pragma unroll
+        for (int tt = 0; tt < 2; ++tt) {
+          const unsigned char* fr = st + FOFF + (2 * warp + tt) * FROW_BYTES + lane * 32;
+          fz[2 * tt] = *reinterpret_cast<const float4*>(fr);
+          fz[2 * tt + 1] = *reinterpret_cast<const float4*>(fr + 16);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);  // this warp has read slot s
+      float2 waa, w1, w2, w3;
+      if (MAPS) {
+        waa = bc(1.f); w1 = bc(-1.f / 64.f); w2 = bc(-1.f / 16.f); w3 = bc(-1.f / 4.f);
+      } else {
+        waa = P.wk[k][0]; w1 = P.wk[k][1]; w2 = P.wk[k][2]; w3 = P.wk[k][3];
+      }
+      const float kk = (float)(P.kbase + k);
+      const float kratio = (kk + 1.f) / kk;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        // vertical: even fine row (h[-1] + 6 h[0] + h[+1]) (/8); odd (h[0] + h[+1]) (/2)
+        const float2 re = pfma(bc(6.f), h[1][q], padd(h[0][q], h[2][q]));
+        const float2 ro = padd(h[1][q], h[2][q]);
+        const float2 we = (q & 1) ? w2 : w1;  // even row: ee 1/64, eo 1/16
+        const float2 wo = (q & 1) ? w3 : w2;  // odd row:  oe 1/16, oo 1/4
+#pragma unroll
+        for (int tt = 0; tt < 2; ++tt) {
+          const int p = 4 * tt + q;
+          const float2 raw = tt == 0 ? re : ro;
+          const float2 w = tt == 0 ? we : wo;
+          float2 V;  // (Im, Re) of a_k (Z_l - up Z_{l+1}) at this pixel
+          float2 zf = make_float2(0.f, 0.f);
+          if (!LEVEL0) {
+            const float4 fv = fz[2 * tt + (q >> 1)];
+            zf = (q & 1) ? hi2(fv) : lo2(fv);
+          }
+          if (MAPS) {
+            V = pmul(bc(mA[p]), LEVEL0 ? pmul(w, raw) : pfma(w, raw, zf));
+          } else {
+            V = LEVEL0 ? pmul(w, raw) : pfma(w, raw, pmul(waa, zf));
+          }
+          // acc += (c V.im, s V.re); result = acc.x - acc.y = a_k Im(e^{-i k w_1 g} (...))
+          acc[p] = pfma(z[p], V, acc[p]);
+          const float2 zn = pfma(bc(-1.f), zp[p], pmul(bc(tc[p]), z[p]));
+          zp[p] = z[p];
+          z[p] = zn;
+          if (MAPS) {
+            mA[p] *= mR[p] * kratio;
+            mR[p] *= mQ[p];
+          }
+        }
+      }
+    }
+
+    float res[8];
+#pragma unroll
+    for (int p = 0; p < 8; ++p) res[p] = acc[p].x - acc[p].y;
+
+    // --- collapse: + up(D_{l+1}) (written by the previous apply grid)
+    if (HAS_D) {
+      if (!waited) {
+        pdl_wait();
+        waited = true;
+        load_d(T, dq);
+      }
+      float hd[3][4];
+#pragma unroll
+      for (int tt = 0; tt < 3; ++tt) {
+        const float x0 = dq[tt][0], x1 = dq[tt][1];
+        const float L = __shfl_up_sync(FULL, x1, 1);
+        const float Rn = __shfl_down_sync(FULL, x0, 1);
+        hd[tt][0] = fmaf(6.f, x0, L + x1) * 0.125f;
+        hd[tt][1] = (x0 + x1) * 0.5f;
+        hd[tt][2] = fmaf(6.f, x1, x0 + Rn) * 0.125f;
+        hd[tt][3] = (x1 + Rn) * 0.5f;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        res[q] += 0.125f * fmaf(6.f, hd[1][q], hd[0][q] + hd[2][q]);
+        res[4 + q] += 0.5f * (hd[1][q] + hd[2][q]);
+      }
+    }
+    if (LEVEL0 && P.include_base) {
+#pragma unroll
+      for (int p = 0; p < 8; ++p) res[p] += g[p];
+    }
+
+    if (act) {
+      const int xf0 = 4 * j;
+      const bool fvec_ok = xf0 + 3 < P.Wf;
+      float* op;
+      long long opitch;
+      bool oal;
+      if (LEVEL0) {
+        op = P.out + T.frame * P.out_fstride;
+        opitch = P.out_pitch;
+        oal = out_al;
+      } else {
+        op = P.fine.D + T.frame * P.fine.fstride_r;
+        opitch = P.fine.pitch;
+        oal = true;
+      }
+#pragma unroll
+      for (int tt = 0; tt < 2; ++tt) {
+        if (2 * r + tt >= P.Hf) break;
+        float* rp = op + (long long)(2 * r + tt) * opitch;
+        if (fvec_ok && oal) {
+          *reinterpret_cast<float4*>(rp + xf0) =
+              make_float4(res[4 * tt], res[4 * tt + 1], res[4 * tt + 2], res[4 * tt + 3]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (xf0 + q < P.Wf) rp[xf0 + q] = res[4 * tt + q];
+        }
+      }
     }
   }
 }
 
-template <typename Kern, typename Par>
-cudaError_t launch_ex(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl, const Par& p) {
+template <typename Kern, typename... Args>
+cudaError_t launch_ex(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl, const Args&... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -717,7 +782,7 @@ cudaError_t launch_ex(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, kern, p);
+  return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
 // Rows per warp strip: long strips amortise the 3 halo rows; shorter strips
@@ -736,7 +801,8 @@ static cudaError_t launch_build_nc(BuildParams p, int batch, cudaStream_t s, boo
   p.nchunks = p.KL / NC;
   p.rows_per_strip = pick_rows(p.Hc, bx, batch * p.nchunks);
   dim3 grid(bx, (p.Hc + p.rows_per_strip - 1) / p.rows_per_strip, batch * p.nchunks);
-  return launch_ex(k_build<NC, 1, FROM_IMAGE>, grid, dim3(32), 0, s, pdl, p);
+  if (p.rows_per_strip == 2) return launch_ex(k_build<NC, 1, FROM_IMAGE, true>, grid, dim3(32), 0, s, pdl, p);
+  return launch_ex(k_build<NC, 1, FROM_IMAGE, false>, grid, dim3(32), 0, s, pdl, p);
 }
 
 // largest channel chunk (<= cap) dividing the local order count
@@ -753,8 +819,8 @@ cudaError_t launch_build(const BuildParams& p0, int level_src, int batch, cudaSt
     p.nchunks = 1;
     p.rows_per_strip = pick_rows(p.Hc, bx, 1);
     dim3 grid(bx, (p.Hc + p.rows_per_strip - 1) / p.rows_per_strip, 1);
-    if (level_src == 0) return launch_ex(k_build<0, 2, true>, grid, dim3(32), 0, s, pdl, p);
-    return launch_ex(k_build<0, 2, false>, grid, dim3(32), 0, s, pdl, p);
+    if (level_src == 0) return launch_ex(k_build<0, 2, true, false>, grid, dim3(32), 0, s, pdl, p);
+    return launch_ex(k_build<0, 2, false, false>, grid, dim3(32), 0, s, pdl, p);
   }
   if (level_src == 0) {
     static const int cap0 = [] {
@@ -786,9 +852,20 @@ cudaError_t launch_build(const BuildParams& p0, int level_src, int batch, cudaSt
   }
 }
 
+static int sm_count() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
 template <bool L0, bool HD, bool MP>
 static cudaError_t launch_apply_t(const ApplyParams& p, int batch, cudaStream_t s, bool pdl) {
-  dim3 grid((p.Wf + 119) / 120, (p.Hc + 3) / 4, batch);
+  const int ntiles = ((p.Wf + 119) / 120) * ((p.Hc + 3) / 4) * batch;
+  const int per_sm = MP ? 2 : 3;  // resident CTAs per SM (launch bounds)
+  dim3 grid(std::min(ntiles, sm_count() * per_sm));
   const int smem = apply_stages<L0>() * apply_stage_bytes<L0>();
   static bool attr_set = false;  // > 48 KB of dynamic shared memory needs an opt-in
   if (!attr_set) {
@@ -796,7 +873,7 @@ static cudaError_t launch_apply_t(const ApplyParams& p, int batch, cudaStream_t 
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  return launch_ex(k_apply<L0, HD, MP>, grid, dim3(160), smem, s, pdl, p);
+  return launch_ex(k_apply<L0, HD, MP>, grid, dim3(160), smem, s, pdl, p, ntiles);
 }
 
 cudaError_t launch_apply(const ApplyParams& p, int level_fine, bool has_d, bool maps, int batch,

@@ -64,6 +64,8 @@ _SIGS = {
     "fllf_coefficients": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, ctypes.c_double,
                                          ctypes.c_double, ctypes.POINTER(ctypes.c_double),
                                          ctypes.POINTER(ctypes.c_double)]),
+    "fllf_optimal_period": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, ctypes.c_double,
+                                           ctypes.POINTER(ctypes.c_double)]),
     "fllf_plan_level_dims": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
                                             ctypes.POINTER(ctypes.c_int)]),
     "fllf_workspace_bytes": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_size_t)]),
@@ -193,6 +195,12 @@ def fllf_coefficients(K, T, sigma_r, m):
     a = (ctypes.c_double * K)()
     _check(lib.fllf_coefficients(K, float(T), float(sigma_r), float(m), om, a))
     return np.array(om[:]), np.array(a[:])
+
+
+def fllf_optimal_period(K, sigma_r, R=256.0) -> float:
+    t = ctypes.c_double()
+    _check(lib.fllf_optimal_period(K, float(sigma_r), float(R), ctypes.byref(t)))
+    return t.value
 
 
 def fllf_plan_level_dims(plan, level):

@@ -43,6 +43,21 @@ def test_host_coefficients_match_oracle():
         np.testing.assert_allclose(a, c["a"], rtol=1e-13)
 
 
+def test_optimal_period_eq12():
+    """NEXT-2 (Eq. 12): host C implementation vs the paper's T = 405.9 for
+    sigma_r = 30 (golden) and vs the oracle's independent search."""
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "period_eq12.json")))
+    T = F.fllf_optimal_period(g["K"], g["sigma_r"], g["R"])
+    assert abs(T - g["paper_T"]) < g["abs_tol"]
+    for K in (2, 6, 10, 16):
+        for sig in (10.0, 30.0, 60.0):
+            assert abs(F.fllf_optimal_period(K, sig, 256.0) - O.optimal_period(K, sig, 256.0)) < 1e-4
+    with pytest.raises(F.FllfError):
+        F.fllf_optimal_period(0, 30.0, 256.0)
+
+
 @pytest.mark.parametrize("args,code", [
     ((0, 10, 3, 4, 510.0, 30.0, 1.0), F.FLLF_ERR_INVALID_ARGUMENT),
     ((10, 10, 1, 4, 510.0, 30.0, 1.0), F.FLLF_ERR_INVALID_ARGUMENT),
