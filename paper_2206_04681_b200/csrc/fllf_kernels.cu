@@ -398,18 +398,18 @@ __global__ void __launch_bounds__(32) k_build(const BuildParams P) {
   if (interior) {
     if (zfirst) {
       BuildWarp<NC, NR, FROM_IMAGE, false, true> w(P, cb, o0, chunk, frame);
-      w.template run<(FROM_IMAGE || SMALL) ? 4 : 2>(R);
+      w.template run<SMALL ? 4 : 2>(R);
     } else {
       BuildWarp<NC, NR, FROM_IMAGE, false, false> w(P, cb, o0, chunk, frame);
-      w.template run<(FROM_IMAGE || SMALL) ? 4 : 2>(R);
+      w.template run<SMALL ? 4 : 2>(R);
     }
   } else {
     if (zfirst) {
       BuildWarp<NC, NR, FROM_IMAGE, true, true> w(P, cb, o0, chunk, frame);
-      w.template run<(FROM_IMAGE || SMALL) ? 4 : 2>(R);
+      w.template run<SMALL ? 4 : 2>(R);
     } else {
       BuildWarp<NC, NR, FROM_IMAGE, true, false> w(P, cb, o0, chunk, frame);
-      w.template run<(FROM_IMAGE || SMALL) ? 4 : 2>(R);
+      w.template run<SMALL ? 4 : 2>(R);
     }
   }
 }

@@ -20,11 +20,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="config2")
     ap.add_argument("--iters", type=int, default=2)
+    ap.add_argument("--frames", type=int, default=16)
     a = ap.parse_args()
     cfg = int(a.workload[-1])
     c = synth.CONFIGS[cfg]
     if cfg == 5:
-        x = synth.config5_frames(16)
+        x = synth.config5_frames(a.frames)
     elif cfg in (3, 4):
         x = synth.config2_image(seed=4000, H=c["H"], W=c["W"])[None]
     else:
