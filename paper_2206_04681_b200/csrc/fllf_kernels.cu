@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(32) k_build(const BuildParams P) {
 // (level 0 stages are 3 KB, level >= 1 stages 11 KB)
 template <bool LEVEL0>
 __host__ __device__ constexpr int apply_stages() {
-  return LEVEL0 ? 8 : 6;
+  return LEVEL0 ? 16 : 6;
 }
 constexpr int CROW_BYTES = 64 * 8;   // 32 lanes x 2 coarse complex values
 constexpr int FROW_BYTES = 128 * 8;  // 32 lanes x 4 fine complex values
@@ -568,8 +568,6 @@ __global__ void __launch_bounds__(160, MAPS ? 2 : 3) k_apply(const ApplyParams P
 
   bool waited = P.wait_first != 0;  // D_{l+1} is readable once the PDL wait returned
   int it = 0;
-  float gnext[8];
-  if ((int)blockIdx.x < ntiles) load_g(apply_tile(blockIdx.x, P), gnext);
 #pragma unroll 1
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const ApplyTile T = apply_tile(t, P);
@@ -577,9 +575,7 @@ __global__ void __launch_bounds__(160, MAPS ? 2 : 3) k_apply(const ApplyParams P
     const int j = T.jb * 30 + lane - 1;  // coarse columns 2j, 2j+1 -> fine columns 4j..4j+3
     const bool act = r < P.Hc && lane >= 1 && lane <= 30 && 4 * j < P.Wf;
     float g[8];
-#pragma unroll
-    for (int p = 0; p < 8; ++p) g[p] = gnext[p];
-    if (t + (int)gridDim.x < ntiles) load_g(apply_tile(t + gridDim.x, P), gnext);  // next tile, early
+    load_g(T, g);
     float dq[3][2];
     if (HAS_D && waited) load_d(T, dq);
 
