@@ -123,6 +123,14 @@ __device__ __forceinline__ void vstep(float2& Pv, float2& Av, float2 ve, float2 
   Pv = pfma(bc(W1), vo, pmul(bc(W2), ve));
 }
 
+// Same step with fixed names: P = pending output o-1 (missing its last tap),
+// A = output o.  After the pair: P <- A + w0 ve + w1 vo (output o, missing its
+// last tap), A <- w2 ve + w1 vo (output o+1).
+__device__ __forceinline__ void vstep_fixed(float2& Pv, float2& Av, float2 ve, float2 vo) {
+  Pv = pfma(bc(W1), vo, pfma(bc(W0), ve, Av));
+  Av = pfma(bc(W1), vo, pmul(bc(W2), ve));
+}
+
 // Horizontal 5-tap + decimation of a finished complex row value held as
 // (a, b) = (fine col 2x, 2x+1), each (Im, Re):
 //   h(x) = w2 f(2x-2) + w1 f(2x-1) + w0 f(2x) + w1 f(2x+1) + w2 f(2x+2)
@@ -165,9 +173,9 @@ struct BuildWarp {
   long long rpitch;
   const float2* zsrc;
   float2* zdst;
-  // two role-swapping accumulators per channel and column half (see vstep)
-  float2 S0c[NCX][2], S1c[NCX][2];
-  float2 S0r[NR], S1r[NR];
+  // two accumulators per channel and column half (see vstep_fixed)
+  float2 Pc[NCX][2], Ac[NCX][2];
+  float2 Pr[NR], Ar[NR];
 
   __device__ __forceinline__ BuildWarp(const BuildParams& P_, int cb, int o0_, int chunk, int frame) : P(P_), o0(o0_) {
     const int lane = threadIdx.x & 31;
@@ -211,9 +219,9 @@ struct BuildWarp {
       zdst = P.dst.Z + frame * P.dst.fstride_z + (long long)k0 * P.dst.kstride_z;
     }
 #pragma unroll
-    for (int i = 0; i < NCX; ++i) S0c[i][0] = S0c[i][1] = S1c[i][0] = S1c[i][1] = make_float2(0.f, 0.f);
+    for (int i = 0; i < NCX; ++i) Pc[i][0] = Pc[i][1] = Ac[i][0] = Ac[i][1] = make_float2(0.f, 0.f);
 #pragma unroll
-    for (int i = 0; i < NR; ++i) S0r[i] = S1r[i] = make_float2(0.f, 0.f);
+    for (int i = 0; i < NR; ++i) Pr[i] = Ar[i] = make_float2(0.f, 0.f);
   }
 
   __device__ __forceinline__ void load_row(int row, Row& d) const {
@@ -246,30 +254,28 @@ struct BuildWarp {
     load_row(r0 + 1, d.o);
   }
 
-  // One channel over a row pair with roles (Pc, Ac).
+  // One channel over a row pair.
   template <bool EMIT, bool ONLY>
-  __device__ __forceinline__ void chan(float2 (&Pc)[2], float2 (&Ac)[2], float2 ea_, float2 eb_, float2 oa,
+  __device__ __forceinline__ void chan(float2 (&Pv)[2], float2 (&Av)[2], float2 ea_, float2 eb_, float2 oa,
                                        float2 ob, float2* q) {
     if (EMIT) {
-      const float2 ea = pfma(bc(W2), ea_, Pc[0]);
-      const float2 eb = pfma(bc(W2), eb_, Pc[1]);
+      const float2 ea = pfma(bc(W2), ea_, Pv[0]);
+      const float2 eb = pfma(bc(W2), eb_, Pv[1]);
       const float2 h = hfilt_c(ea, eb);
       if (store_lane) q[0] = h;
       if (halo_l) q[-2] = h;  // x == 1: column -1
       if (halo_r) q[hoff_r] = h;
     }
     if (!ONLY) {
-      vstep(Pc[0], Ac[0], ea_, oa);
-      vstep(Pc[1], Ac[1], eb_, ob);
+      vstep_fixed(Pv[0], Av[0], ea_, oa);
+      vstep_fixed(Pv[1], Av[1], eb_, ob);
     }
   }
 
-  // One row pair with roles (Pc/Pr pending output, Ac/Ar current output).
-  // EMIT: finish output row `emit` with the even row and store it; ONLY: the
-  // final row (no accumulator update).
+  // One row pair.  EMIT: finish output row `emit` with the even row and
+  // store it; ONLY: the final row (no accumulator update).
   template <bool EMIT, bool ONLY>
-  __device__ __forceinline__ void proc(const Pair& d, float2 (&Pc)[NCX][2], float2 (&Ac)[NCX][2],
-                                       float2 (&Pr)[NR], float2 (&Ar)[NR], int emit) {
+  __device__ __forceinline__ void proc(const Pair& d, int emit) {
     if (do_real) {
 #pragma unroll
       for (int i = 0; i < NR; ++i) {
@@ -278,7 +284,7 @@ struct BuildWarp {
           const float h = hfilt_r(e.x, e.y);
           if (store_lane) rdst[i][(long long)emit * P.dst.pitch + x] = h;
         }
-        if (!ONLY) vstep(Pr[i], Ar[i], d.e.r[i], d.o.r[i]);
+        if (!ONLY) vstep_fixed(Pr[i], Ar[i], d.e.r[i], d.o.r[i]);
       }
     }
     if (NC == 0) return;
@@ -331,48 +337,66 @@ struct BuildWarp {
     }
   }
 
-  // Stream the strip: pairs 0 (halo rows) .. R (last output pairs) and the
-  // final row (even row of pair R+1), keeping PD row pairs in flight.  Pair p
-  // lives in buf[p % PD] and uses roles (S1, S0) for even p, (S0, S1) for odd
-  // p; PD is even so both are compile-time inside the unrolled bodies.
-  template <int PD>
+  // Stream the strip: pairs 0 (halo rows) .. R and the final row (even row of
+  // pair R+1).  ROTATE: one pair per iteration with a two-buffer rotation
+  // (small loop body; the rotation copies only the prefetched row data, cheap
+  // at level 0).  Otherwise two pairs per iteration with static buffers.
+  template <bool ROTATE>
   __device__ __forceinline__ void run(int R) {
-    static_assert(PD % 2 == 0 && PD >= 2, "PD must be even");
-    Pair buf[PD];
-#pragma unroll
-    for (int i = 0; i < PD; ++i) load_pair(i, buf[i]);
-    proc<false, false>(buf[0], S1c, S0c, S1r, S0r, 0);  // p = 0: halo rows
-    load_pair(PD, buf[0]);
-    proc<false, false>(buf[1], S0c, S1c, S0r, S1r, 0);  // p = 1: first pair, nothing to emit
-    load_pair(PD + 1, buf[1]);
-    int p = 2;
+    if (ROTATE) {
+      Pair cur, nxt;
+      load_pair(0, cur);
+      load_pair(1, nxt);
+      proc<false, false>(cur, 0);  // p = 0: halo rows
+      cur = nxt;
+      load_pair(2, nxt);
+      proc<false, false>(cur, 0);  // p = 1: first pair, nothing to emit
+      cur = nxt;
+      load_pair(3, nxt);
 #pragma unroll 1
-    for (; p + PD - 1 <= R; p += PD) {
-#pragma unroll
-      for (int i = 0; i < PD; ++i) {
-        if ((i & 1) == 0)
-          proc<true, false>(buf[(2 + i) % PD], S1c, S0c, S1r, S0r, o0 + p + i - 2);
-        else
-          proc<true, false>(buf[(2 + i) % PD], S0c, S1c, S0r, S1r, o0 + p + i - 2);
-        load_pair(p + i + PD, buf[(2 + i) % PD]);
+      for (int p = 2; p <= R; ++p) {
+        proc<true, false>(cur, o0 + p - 2);
+        cur = nxt;
+        load_pair(p + 2, nxt);
+      }
+      proc<true, true>(cur, o0 + R - 1);
+    } else {
+      Pair BA, BB;
+      load_pair(0, BA);
+      load_pair(1, BB);
+      proc<false, false>(BA, 0);
+      load_pair(2, BA);
+      proc<false, false>(BB, 0);
+      load_pair(3, BB);
+      int p = 2;
+#pragma unroll 1
+      for (; p + 1 <= R; p += 2) {
+        proc<true, false>(BA, o0 + p - 2);
+        load_pair(p + 2, BA);
+        proc<true, false>(BB, o0 + p - 1);
+        load_pair(p + 3, BB);
+      }
+      if (p <= R) {
+        proc<true, false>(BA, o0 + p - 2);
+        proc<true, true>(BB, o0 + R - 1);
+      } else {
+        proc<true, true>(BA, o0 + R - 1);
       }
     }
-    // fewer than PD pairs left, then the final row (pair R+1)
-#pragma unroll
-    for (int i = 0; i < PD; ++i) {
-      const int pp = p + i;
-      if (pp <= R) {
-        if ((i & 1) == 0)
-          proc<true, false>(buf[(2 + i) % PD], S1c, S0c, S1r, S0r, o0 + pp - 2);
-        else
-          proc<true, false>(buf[(2 + i) % PD], S0c, S1c, S0r, S1r, o0 + pp - 2);
-      } else if (pp == R + 1) {
-        if ((i & 1) == 0)
-          proc<true, true>(buf[(2 + i) % PD], S1c, S0c, S1r, S0r, o0 + R - 1);
-        else
-          proc<true, true>(buf[(2 + i) % PD], S0c, S1c, S0r, S1r, o0 + R - 1);
-      }
-    }
+  }
+
+  // Strips of exactly 2 output rows (tiny levels): every input row is loaded
+  // up front, one memory round trip.
+  __device__ __forceinline__ void run2() {
+    Pair B0, B1, B2, B3;
+    load_pair(0, B0);
+    load_pair(1, B1);
+    load_pair(2, B2);
+    load_pair(3, B3);
+    proc<false, false>(B0, 0);
+    proc<false, false>(B1, 0);
+    proc<true, false>(B2, o0);
+    proc<true, true>(B3, o0 + 1);
   }
 };
 
@@ -401,18 +425,18 @@ __global__ void __launch_bounds__(32) k_build(const BuildParams P) {
   if (interior) {
     if (zfirst) {
       BuildWarp<NC, NR, FROM_IMAGE, false, true> w(P, cb, o0, chunk, frame);
-      w.template run<SMALL ? 4 : 2>(R);
+      if (SMALL && R == 2) w.run2(); else w.template run<FROM_IMAGE>(R);
     } else {
       BuildWarp<NC, NR, FROM_IMAGE, false, false> w(P, cb, o0, chunk, frame);
-      w.template run<SMALL ? 4 : 2>(R);
+      if (SMALL && R == 2) w.run2(); else w.template run<FROM_IMAGE>(R);
     }
   } else {
     if (zfirst) {
       BuildWarp<NC, NR, FROM_IMAGE, true, true> w(P, cb, o0, chunk, frame);
-      w.template run<SMALL ? 4 : 2>(R);
+      if (SMALL && R == 2) w.run2(); else w.template run<FROM_IMAGE>(R);
     } else {
       BuildWarp<NC, NR, FROM_IMAGE, true, false> w(P, cb, o0, chunk, frame);
-      w.template run<SMALL ? 4 : 2>(R);
+      if (SMALL && R == 2) w.run2(); else w.template run<FROM_IMAGE>(R);
     }
   }
 }
