@@ -409,11 +409,12 @@ __global__ void __launch_bounds__(32) k_build(const BuildParams P) {
   const int o0 = blockIdx.y * P.rows_per_strip;
   if (o0 >= P.Hc) return;
   const int R = min(P.rows_per_strip, P.Hc - o0);
-  // chunk-major: CTAs are dispatched in blockIdx order, so resident warps
-  // mostly run the same code variant (instruction-cache locality)
+  // level 0: chunk-major (CTAs are dispatched in blockIdx order, so resident
+  // warps mostly run the same code variant -- instruction-cache locality);
+  // above: frame-major (L2 locality of the shared G plane)
   const int nframes = gridDim.z / P.nchunks;
-  const int chunk = blockIdx.z / nframes;
-  const int frame = blockIdx.z % nframes;
+  const int chunk = FROM_IMAGE ? blockIdx.z / nframes : blockIdx.z % P.nchunks;
+  const int frame = FROM_IMAGE ? blockIdx.z % nframes : blockIdx.z / P.nchunks;
   // are all 64 fine columns of this warp inside the row (and, for the
   // caller's image, 8-byte aligned)?
   bool interior = (60 * cb - 2 >= 0) && (60 * cb + 61 < P.Wf);

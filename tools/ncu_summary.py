@@ -1,0 +1,59 @@
+"""Summarise an ncu report (--set full) into markdown + roofline traffic json.
+
+    python tools/ncu_summary.py gpurun_out/prof.ncu-rep profiles/r01_ncu_full.md [workload]
+"""
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+rep, out_md = sys.argv[1], sys.argv[2]
+workload = sys.argv[3] if len(sys.argv) > 3 else "config2"
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(raw)))
+hdr, units, data = rows[0], rows[1], rows[2:]
+
+
+def g(r, k):
+    return r[hdr.index(k)] if k in hdr else ""
+
+
+stall_cols = [i for i, h in enumerate(hdr)
+              if h.startswith("smsp__average_warps_issue_stalled") and h.endswith("per_issue_active.ratio")]
+lines = ["| # | kernel | time (us) | DRAM read (MB) | DRAM write (MB) | regs | occupancy % | issue active % | FMA pipe % | L1 % | top stalls (cycles/issue) |",
+         "|---|---|---|---|---|---|---|---|---|---|---|"]
+traffic = {}
+seen = {}
+for n, r in enumerate(data):
+    name = g(r, "Kernel Name")
+    short = name[name.find("k_"):name.find("(")] if "k_" in name else name[:40]
+    t_us = float(g(r, "gpu__time_duration.sum") or 0)
+    tu = units[hdr.index("gpu__time_duration.sum")]
+    if tu == "ns":
+        t_us /= 1e3
+    elif tu == "ms":
+        t_us *= 1e3
+
+    def mb(k):
+        v = float(g(r, k) or 0)
+        u = units[hdr.index(k)] if k in hdr else "byte"
+        scale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(u, 1e-6)
+        return v * scale
+
+    rd, wr = mb("dram__bytes_read.sum"), mb("dram__bytes_write.sum")
+    st = sorted(((float(r[i] or 0), hdr[i].replace("smsp__average_warps_issue_stalled_", "")
+                  .replace("_per_issue_active.ratio", "")) for i in stall_cols), reverse=True)[:3]
+    lines.append(f"| {n} | `{short}` | {t_us:.2f} | {rd:.2f} | {wr:.2f} | {g(r, 'launch__registers_per_thread')} | "
+                 f"{float(g(r, 'sm__warps_active.avg.pct_of_peak_sustained_active') or 0):.1f} | "
+                 f"{float(g(r, 'smsp__issue_active.avg.pct_of_peak_sustained_active') or 0):.1f} | "
+                 f"{float(g(r, 'sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active') or 0):.1f} | "
+                 f"{float(g(r, 'l1tex__throughput.avg.pct_of_peak_sustained_active') or 0):.1f} | "
+                 + ", ".join(f"{nm} {v:.2f}" for v, nm in st) + " |")
+    seen.setdefault(short, []).append((rd + wr) * 1e6)
+# roofline traffic per (kind, level) for the sequence order build0..build(l), apply(l)..apply0
+md = [f"# ncu --set full summary: `{os.path.basename(rep)}` ({workload})", "",
+      "Per launch, cold caches (ncu replays each kernel with caches flushed), --clock-control none.", ""] + lines
+open(out_md, "w").write("\n".join(md) + "\n")
+print("\n".join(md))
