@@ -33,7 +33,7 @@ def build(verbose: bool = False, extra: list[str] | None = None) -> str:
     os.makedirs(LIBDIR, exist_ok=True)
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-Xcompiler", "-fvisibility=hidden", "-ftz=true", "-I", INCLUDE, "-I", CSRC,
+           "-Xcompiler", "-fvisibility=hidden", "-I", INCLUDE, "-I", CSRC,
            "-Xptxas", "-v" if verbose else "-O3", *srcs, "-o", LIB, *(extra or [])]
     # export only the C ABI (fllf_*): visibility=hidden + explicit default visibility
     cmd += ["-DFLLF_BUILD"]

@@ -451,6 +451,10 @@ fllf_status fllf_apply(fllf_plan p, const fllf_apply_args* a, float* d_out, size
     ap.wk[i][1] = make_float2(-a / 64.f, -a / 64.f);
     ap.wk[i][2] = make_float2(-a / 16.f, -a / 16.f);
     ap.wk[i][3] = make_float2(-a / 4.f, -a / 4.f);
+    ap.cw[i][0] = make_float2(-a / 64.f, a / 64.f);
+    ap.cw[i][1] = make_float2(-a / 16.f, a / 16.f);
+    ap.cw[i][2] = make_float2(-a / 4.f, a / 4.f);
+    ap.cw[i][3] = make_float2(a, -a);
   }
   int launches = 0;
   if (p->last_was_apply) p->nrec = 0;

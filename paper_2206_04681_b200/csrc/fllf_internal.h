@@ -77,6 +77,12 @@ struct ApplyParams {
   // [3] = -(a/4) (odd row, odd col): the polyphase up-sampling scales folded
   // into a_k
   float2 wk[FLLF_MAX_K][4];
+  // Clenshaw form (k_apply_cl): per local order k the coefficient pairs that
+  // turn an up-sampled (Im, Re) value into (c_cos, c_sin) of the trig series
+  // sum_k (c_cos cos k theta + c_sin sin k theta):
+  // [0] = (-a/64, a/64) even row, even col; [1] = (-a/16, a/16) mixed;
+  // [2] = (-a/4, a/4) odd row, odd col; [3] = (a, -a) same-level Z (l >= 1).
+  float2 cw[FLLF_MAX_K][4];
 };
 
 // Kernel launchers (fllf_kernels.cu).  Return cudaGetLastError() after launch.

@@ -442,6 +442,194 @@ __global__ void __launch_bounds__(32) k_build(const BuildParams P) {
   }
 }
 
+// --------------------------------------------------------------- build0 v2
+// Level-0 build (steps a2 + a3 from the image): same warp geometry as k_build
+// (lane = fine columns 2x, 2x+1 -> coarse column x; 30 outputs per warp;
+// vertical 5-tap first over row pairs, horizontal on the finished row with
+// warp shuffles), restructured for issue efficiency:
+//  * integer binomial weights [1,4,6,4,1] in both passes, the (1/16)^2 folded
+//    into the phasor amplitude (complex channels) or one multiply at emit (G);
+//  * the order recurrence z_{k+1} = 2 cos(theta) z_k - z_{k-1} is ONE packed
+//    FFMA2 per pixel (negated addend);
+//  * up to 8 orders per warp (amortises the per-pixel sincos + chunk-start
+//    phasor); I rows prefetched PD pairs ahead;
+//  * 32-bit in-frame offsets; halo-column stores only in edge warps.
+template <int NC, bool EDGE>
+struct Build0Warp {
+  const BuildParams& P;
+  int o0, x, c0, rc0, rc1;
+  bool store_lane, halo_l, halo_r, do_real, zfirst;
+  int g0;
+  const float* isrc;
+  long long ipitch;
+  float* gdst;
+  float2* zdst;  // channel 0 of this chunk, frame base
+  float2 Pc[NC][2], Ac[NC][2];
+  float2 Pr, Ar;
+
+  __device__ __forceinline__ Build0Warp(const BuildParams& P_, int cb, int o0_, int chunk, int frame)
+      : P(P_), o0(o0_) {
+    const int lane = threadIdx.x & 31;
+    x = cb * 30 + lane - 1;
+    store_lane = lane >= 1 && lane <= 30 && x < P.Wc;
+    c0 = 2 * x;
+    rc0 = EDGE ? refl101(c0, P.Wf) : c0;
+    rc1 = EDGE ? refl101(c0 + 1, P.Wf) : c0 + 1;
+    g0 = P.kbase + chunk * NC;
+    zfirst = g0 == 1;  // chunks starting at order 1 need no chunk-start phasor
+    do_real = chunk == 0;
+    halo_l = EDGE && store_lane && x == 1;
+    halo_r = EDGE && store_lane && x == ((P.Wf & 1) ? P.Wc - 2 : P.Wc - 1);
+    isrc = P.img.p + frame * P.img.fstride;
+    ipitch = P.img.pitch;
+    gdst = P.dst.G + frame * P.dst.fstride_r;
+    zdst = P.dst.Z + frame * P.dst.fstride_z + (long long)(chunk * NC) * P.dst.kstride_z;
+#pragma unroll
+    for (int i = 0; i < NC; ++i) Pc[i][0] = Pc[i][1] = Ac[i][0] = Ac[i][1] = make_float2(0.f, 0.f);
+    Pr = Ar = make_float2(0.f, 0.f);
+  }
+
+  // the two image pixels of fine row `row` (reflect-101)
+  __device__ __forceinline__ float2 load_row(int row) const {
+    const float* rp = isrc + (long long)refl101(row, P.Hf) * ipitch;
+    return EDGE ? make_float2(__ldg(rp + rc0), __ldg(rp + rc1)) : ldg2(rp + c0);
+  }
+  struct Pair {
+    float2 e, o;  // even / odd fine row, (col a, col b)
+  };
+  // pair p holds rows 2(o0+p-1), 2(o0+p-1)+1 (p = 0: the two halo rows above)
+  __device__ __forceinline__ void load_pair(int p, Pair& d) const {
+    const int r0 = 2 * (o0 + p - 1);
+    d.e = load_row(r0);
+    d.o = load_row(r0 + 1);
+  }
+
+  // horizontal [1,4,6,4,1] + decimation of a finished row (complex), a = col 2x, b = 2x+1
+  __device__ __forceinline__ static float2 hsum_c(float2 a, float2 b) {
+    const float2 La = shfl_up2(a), Lb = shfl_up2(b), Ra = shfl_down2(a);
+    return pfma(bc(6.f), a, pfma(bc(4.f), padd(b, Lb), padd(La, Ra)));
+  }
+
+  template <bool EMIT, bool ONLY>
+  __device__ __forceinline__ void proc(const Pair& d, int emit) {
+    if (do_real) {
+      // G channel, packed over the two columns
+      if (EMIT) {
+        const float2 e = padd(Pr, d.e);
+        const float a = e.x, b = e.y;
+        const float La = __shfl_up_sync(FULL, a, 1), Lb = __shfl_up_sync(FULL, b, 1);
+        const float Ra = __shfl_down_sync(FULL, a, 1);
+        const float h = fmaf(6.f, a, fmaf(4.f, b + Lb, La + Ra)) * (1.f / 256.f);
+        if (store_lane) gdst[emit * P.dst.pitch + x] = h;
+      }
+      if (!ONLY) {
+        Pr = pfma(bc(6.f), d.e, pfma(bc(4.f), d.o, Ar));
+        Ar = pfma(bc(4.f), d.o, d.e);
+      }
+    }
+    // phasors of the 4 pixels (even/odd row x col a/b), (Im, Re) = (sin, cos),
+    // amplitude 1/256 (the binomial normalisation of both passes)
+    const float I4[4] = {d.e.x, d.e.y, d.o.x, d.o.y};
+    float2 zc[4], zp[4];
+    float tc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      float sn, cs;
+      sincos_turns(I4[u], P.invT, &sn, &cs);
+      tc[u] = 2.f * cs;
+      if (zfirst) {
+        zp[u] = make_float2(0.f, 1.f / 256.f);
+        zc[u] = make_float2(sn * (1.f / 256.f), cs * (1.f / 256.f));
+      } else {
+        float sg, cg;
+        sincos_turns_n(I4[u], P.invT, g0, &sg, &cg);
+        sg *= 1.f / 256.f;
+        cg *= 1.f / 256.f;
+        zc[u] = make_float2(sg, cg);
+        zp[u] = make_float2(fmaf(sg, cs, -cg * sn), fmaf(cg, cs, sg * sn));  // e^{i (g0-1) theta}
+      }
+    }
+    const int off0 = emit * P.dst.zpitch + x;  // in-frame float2 offset of (emit, x), channel 0
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      if (EMIT) {
+        const float2 ea = padd(Pc[i][0], zc[0]);
+        const float2 eb = padd(Pc[i][1], zc[1]);
+        const float2 h = hsum_c(ea, eb);
+        float2* q = zdst + (off0 + i * (int)P.dst.kstride_z);
+        if (store_lane) q[0] = h;
+        if (EDGE) {
+          if (halo_l) q[-2] = h;  // x == 1: column -1
+          if (halo_r) q[P.Wc - x] = h;
+        }
+      }
+      if (!ONLY) {
+        Pc[i][0] = pfma(bc(6.f), zc[0], pfma(bc(4.f), zc[2], Ac[i][0]));
+        Pc[i][1] = pfma(bc(6.f), zc[1], pfma(bc(4.f), zc[3], Ac[i][1]));
+        Ac[i][0] = pfma(bc(4.f), zc[2], zc[0]);
+        Ac[i][1] = pfma(bc(4.f), zc[3], zc[1]);
+      }
+      if (i + 1 < NC) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float2 zn = pfma(bc(tc[u]), zc[u], pneg(zp[u]));
+          zp[u] = zc[u];
+          zc[u] = zn;
+        }
+      }
+    }
+  }
+
+  // Stream the strip: pairs 0 (halo rows) .. R and the final row (even row of
+  // pair R+1); two pairs per iteration with static buffers (the next two
+  // pairs are in flight while one is processed).
+  __device__ __forceinline__ void run(int R) {
+    Pair BA, BB;
+    load_pair(0, BA);
+    load_pair(1, BB);
+    proc<false, false>(BA, 0);
+    load_pair(2, BA);
+    proc<false, false>(BB, 0);
+    load_pair(3, BB);
+    int p = 2;
+#pragma unroll 1
+    for (; p + 1 <= R; p += 2) {
+      proc<true, false>(BA, o0 + p - 2);
+      load_pair(p + 2, BA);
+      proc<true, false>(BB, o0 + p - 1);
+      load_pair(p + 3, BB);
+    }
+    if (p <= R) {
+      proc<true, false>(BA, o0 + p - 2);
+      proc<true, true>(BB, o0 + R - 1);
+    } else {
+      proc<true, true>(BA, o0 + R - 1);
+    }
+  }
+};
+
+template <int NC>
+__global__ void __launch_bounds__(32) k_build0(const BuildParams P) {
+  pdl_trigger();
+  const int cb = blockIdx.x;
+  if (cb * 30 >= P.Wc) return;
+  const int o0 = blockIdx.y * P.rows_per_strip;
+  if (o0 >= P.Hc) return;
+  const int R = min(P.rows_per_strip, P.Hc - o0);
+  const int nframes = gridDim.z / P.nchunks;
+  const int chunk = blockIdx.z / nframes;
+  const int frame = blockIdx.z % nframes;
+  bool interior = (60 * cb - 2 >= 0) && (60 * cb + 61 < P.Wf);
+  interior = interior && ((reinterpret_cast<uintptr_t>(P.img.p) & 7) == 0) && ((P.img.pitch & 1) == 0);
+  if (interior) {
+    Build0Warp<NC, false> w(P, cb, o0, chunk, frame);
+    w.run(R);
+  } else {
+    Build0Warp<NC, true> w(P, cb, o0, chunk, frame);
+    w.run(R);
+  }
+}
+
 // ----------------------------------------------------------------- apply
 // TMA ring depth: enough stages in flight to cover the L2/HBM round trip
 // (level 0 stages are 3 KB, level >= 1 stages 11 KB)
@@ -794,6 +982,398 @@ __global__ void __launch_bounds__(160, MAPS ? 2 : 3) k_apply(const ApplyParams P
   }
 }
 
+// --------------------------------------------------------- apply (Clenshaw)
+// Uniform coefficients (SCALAR / COEFFS).  Same tiles and warp roles as
+// k_apply, but the producer streams the orders in DESCENDING k and the
+// consumers evaluate the order sum with Clenshaw's recurrence instead of
+// carrying the phasors e^{i k theta} forward: with c_k = (c_cos, c_sin) the
+// per-order coefficient pair of a pixel,
+//   b_k = c_k + 2 cos(theta) b_{k+1} - b_{k+2},   b_{k1+1} = b_{k1+2} = 0,
+//   sum_{k=k0}^{k1} (c_cos,k cos k theta + c_sin,k sin k theta)
+//     = b_{k0} . (cos k0 theta, sin k0 theta) - b_{k0+1} . (cos (k0-1) theta, sin (k0-1) theta)
+// (cos k theta and sin k theta both satisfy phi_{k+1} = 2 cos theta phi_k - phi_{k-1}).
+// Per pixel and order that is two packed FFMA2 (one with a negated addend) at
+// level 0, three at l >= 1 (same-level Z term), instead of the phasor update
+// plus accumulate.  The up-sampling is done vertically first: per coarse
+// column the even fine row takes (x_{r-1} + 6 x_r + x_{r+1}), the odd one
+// (x_r + x_{r+1}); the horizontal polyphase step then needs only the two
+// neighbour columns of those two values (4 complex shuffles per order).
+// The polyphase scales 1/64, 1/16, 1/4 and the sign pattern of
+// Im(e^{-i k theta} V) = cos k theta V_im - sin k theta V_re are folded into
+// P.cw (see ApplyParams).
+//
+// Tile header (double-buffered, staged by the producer like the order stages):
+// the 8 fine rows of g (I at level 0, G_l above; 120 fine columns from 120 jb)
+// and the 6 coarse rows of D_{l+1} (68 columns from 60 jb - 4, 16-byte
+// aligned; the up-sampling border rule is applied when the consumers index it).
+constexpr int HDR_G_ROW = 480;
+constexpr int HDR_D_ROW = 272;
+constexpr int HDR_D_OFF = 8 * HDR_G_ROW;
+constexpr int HDR_BYTES = 5504;  // 8*480 + 6*272 = 5472, rounded to 128
+static_assert(HDR_D_OFF + 6 * HDR_D_ROW <= HDR_BYTES, "tile header layout");
+
+// Orders per ring stage (level 0: two, which halves the barrier and index
+// bookkeeping per order) and ring depth.
+template <bool LEVEL0>
+__host__ __device__ constexpr int apply_cl_ops() {
+  return LEVEL0 ? 2 : 1;
+}
+template <bool LEVEL0>
+__host__ __device__ constexpr int apply_cl_stages() {
+  return LEVEL0 ? 8 : 5;
+}
+template <bool LEVEL0>
+__host__ __device__ constexpr int apply_cl_smem() {
+  return apply_cl_stages<LEVEL0>() * apply_cl_ops<LEVEL0>() * apply_stage_bytes<LEVEL0>() + 2 * HDR_BYTES;
+}
+
+template <bool LEVEL0, bool HAS_D>
+__global__ void __launch_bounds__(160, 3) k_apply_cl(const ApplyParams P, const int ntiles) {
+  constexpr int S = apply_cl_stages<LEVEL0>();
+  constexpr int OPS = apply_cl_ops<LEVEL0>();
+  constexpr int OBYTES = apply_stage_bytes<LEVEL0>();  // one order
+  constexpr int STAGE = OPS * OBYTES;
+  constexpr int FOFF = 6 * CROW_BYTES;
+  constexpr int HOFF = S * STAGE;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t full[S];
+  __shared__ __align__(8) uint64_t empty[S];
+  __shared__ __align__(8) uint64_t gfull[2], dfull[2], hempty[2];
+
+  if (P.wait_first) pdl_wait();
+  pdl_trigger();
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int KL = P.KL;
+  // g rows by TMA: internal planes always; the caller's image when its rows
+  // are 16-byte aligned and W is a multiple of 4 (copies never leave a row)
+  const bool tma_g = !LEVEL0 || (((reinterpret_cast<uintptr_t>(P.img.p) & 15) == 0) &&
+                                 ((P.img.pitch & 3) == 0) && ((P.Wf & 3) == 0));
+
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 4);
+    }
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&gfull[b], 1);
+      mbar_init(&dfull[b], 1);
+      mbar_init(&hempty[b], 4);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == 4) {
+    // ---- producer (whole warp, uniform control flow; one elected lane
+    // issues).  Per tile: g rows, the order stages k = KL-1 .. 0 (6 coarse row
+    // segments of Z_{l+1,k} + 8 fine row segments of Z_{l,k}), then the D rows
+    // (after the PDL wait: D_{l+1} is the previous grid's output).
+    int s = 0;
+    uint32_t ph = 0;
+    int n = 0, nt = 0;
+    bool waited = P.wait_first != 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
+      const ApplyTile T = apply_tile(t, P);
+      const int hb = nt & 1;
+      unsigned char* hdr = smem + HOFF + hb * HDR_BYTES;
+      if (nt >= 2) mbar_wait_parity(&hempty[hb], ((nt >> 1) & 1) ^ 1u);
+      if (tma_g) {
+        const float* gb;
+        long long gp;
+        int wlim;
+        if (LEVEL0) {
+          gb = P.img.p + T.frame * P.img.fstride;
+          gp = P.img.pitch;
+          wlim = P.Wf;
+        } else {
+          gb = P.fine.G + T.frame * P.fine.fstride_r;
+          gp = P.fine.pitch;
+          wlim = P.fine.pitch;
+        }
+        const uint32_t gbytes = (uint32_t)min(HDR_G_ROW, (wlim - 120 * T.jb) * 4);
+        if (elect_one()) {
+          mbar_arrive_expect_tx(&gfull[hb], 8 * gbytes);
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            tma_load_1d(hdr + q * HDR_G_ROW, gb + (long long)min(2 * T.r0 + q, P.Hf - 1) * gp + 120 * T.jb, gbytes,
+                        &gfull[hb]);
+        }
+        __syncwarp();
+      }
+      const float2* zc0 = P.coarse.Z + T.frame * P.coarse.fstride_z + (60 * T.jb - 2);
+      int crow[6];
+#pragma unroll
+      for (int q = 0; q < 6; ++q) crow[q] = upmap(T.r0 - 1 + q, P.Hc, P.Hf);
+      const float2* zf0 = LEVEL0 ? nullptr : P.fine.Z + T.frame * P.fine.fstride_z + (120 * T.jb - 4);
+#pragma unroll 1
+      for (int i = KL - 1; i >= 0; i -= OPS) {
+        if (n >= S) mbar_wait_parity(&empty[s], ph ^ 1u);
+        unsigned char* st = smem + s * STAGE;
+        const int no = min(OPS, i + 1);  // orders in this stage: i, i-1, ...
+        if (elect_one()) {
+          mbar_arrive_expect_tx(&full[s], no * OBYTES);
+#pragma unroll
+          for (int h = 0; h < OPS; ++h) {
+            if (h < no) {
+              const float2* zc = zc0 + (long long)(i - h) * P.coarse.kstride_z;
+              unsigned char* so = st + h * OBYTES;
+#pragma unroll
+              for (int q = 0; q < 6; ++q)
+                tma_load_1d(so + q * CROW_BYTES, zc + (long long)crow[q] * P.coarse.zpitch, CROW_BYTES, &full[s]);
+              if (!LEVEL0) {
+                const float2* zf = zf0 + (long long)(i - h) * P.fine.kstride_z;
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                  tma_load_1d(so + FOFF + q * FROW_BYTES,
+                              zf + (long long)min(2 * T.r0 + q, P.Hf - 1) * P.fine.zpitch, FROW_BYTES, &full[s]);
+              }
+            }
+          }
+        }
+        __syncwarp();
+        ++n;
+        if (++s == S) {
+          s = 0;
+          ph ^= 1u;
+        }
+      }
+      if (HAS_D) {
+        if (!waited) {
+          pdl_wait();
+          waited = true;
+        }
+        const float* db = P.coarse.D + T.frame * P.coarse.fstride_r + (60 * T.jb - 4);
+        if (elect_one()) {
+          mbar_arrive_expect_tx(&dfull[hb], 6 * HDR_D_ROW);
+#pragma unroll
+          for (int q = 0; q < 6; ++q)
+            tma_load_1d(hdr + HDR_D_OFF + q * HDR_D_ROW, db + (long long)crow[q] * P.coarse.pitch, HDR_D_ROW,
+                        &dfull[hb]);
+        }
+        __syncwarp();
+      }
+    }
+    return;
+  }
+
+  // ---- consumers
+  const bool out_al = ((reinterpret_cast<uintptr_t>(P.out) & 15) == 0) && ((P.out_pitch & 3) == 0);
+  const unsigned char* rowc = smem + warp * CROW_BYTES + lane * 16;              // coarse row r-1 of this warp
+  const unsigned char* rowf = smem + FOFF + 2 * warp * FROW_BYTES + lane * 32;  // fine row 2r
+  const int lg = min(max(lane - 1, 0), 29);  // header g column block of this lane (halo lanes: any)
+  int s = 0;
+  uint32_t ph = 0;
+  int nt = 0;
+#pragma unroll 1
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
+    const ApplyTile T = apply_tile(t, P);
+    const int hb = nt & 1;
+    const uint32_t hph = (nt >> 1) & 1;
+    const unsigned char* hdr = smem + HOFF + hb * HDR_BYTES;
+    const int r = T.r0 + warp;
+    const int j = T.jb * 30 + lane - 1;  // coarse columns 2j, 2j+1 -> fine columns 4j..4j+3
+    const bool act = r < P.Hc && lane >= 1 && lane <= 30 && 4 * j < P.Wf;
+    float g[8];
+    if (tma_g) {
+      mbar_wait_parity(&gfull[hb], hph);
+#pragma unroll
+      for (int tt = 0; tt < 2; ++tt) {
+        const float4 v = *reinterpret_cast<const float4*>(hdr + (2 * warp + tt) * HDR_G_ROW + lg * 16);
+        g[4 * tt + 0] = v.x; g[4 * tt + 1] = v.y; g[4 * tt + 2] = v.z; g[4 * tt + 3] = v.w;
+      }
+    } else {  // caller image not TMA-compatible: direct loads (level 0 only)
+      const int rr = min(r, P.Hc - 1);
+      const int xf0 = 4 * j;
+      const float* base = P.img.p + T.frame * P.img.fstride;
+#pragma unroll
+      for (int tt = 0; tt < 2; ++tt) {
+        const float* rp = base + (long long)min(2 * rr + tt, P.Hf - 1) * P.img.pitch;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) g[4 * tt + q] = __ldg(rp + min(max(xf0 + q, 0), P.Wf - 1));
+      }
+    }
+    float tc[8], sn[8];
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      float c;
+      sincos_turns(g[p], P.invT, &sn[p], &c);
+      tc[p] = 2.f * c;
+    }
+    float2 b1[8], b2[8];
+#pragma unroll
+    for (int p = 0; p < 8; ++p) b1[p] = b2[p] = make_float2(0.f, 0.f);
+
+    // one order from stage slot `so` (order-local base): bn holds b_{k+2} on
+    // entry and b_k on exit, bp = b_{k+1}
+    auto order = [&](int i, const unsigned char* so, float2 (&bn)[8], const float2 (&bp)[8]) {
+      const float4 x0 = *reinterpret_cast<const float4*>(so);
+      const float4 x1 = *reinterpret_cast<const float4*>(so + CROW_BYTES);
+      const float4 x2 = *reinterpret_cast<const float4*>(so + 2 * CROW_BYTES);
+      float4 fz[4];
+      if (!LEVEL0) {
+        const unsigned char* sf = so + (rowf - rowc);
+        fz[0] = *reinterpret_cast<const float4*>(sf);
+        fz[1] = *reinterpret_cast<const float4*>(sf + 16);
+        fz[2] = *reinterpret_cast<const float4*>(sf + FROW_BYTES);
+        fz[3] = *reinterpret_cast<const float4*>(sf + FROW_BYTES + 16);
+      }
+      // vertical: even fine row (x_{r-1} + 6 x_r + x_{r+1}), odd (x_r + x_{r+1}); columns a = 2j, b = 2j+1
+      const float2 vea = pfma(bc(6.f), lo2(x1), padd(lo2(x0), lo2(x2)));
+      const float2 veb = pfma(bc(6.f), hi2(x1), padd(hi2(x0), hi2(x2)));
+      const float2 voa = padd(lo2(x1), lo2(x2));
+      const float2 vob = padd(hi2(x1), hi2(x2));
+      const float2 Le = shfl_up2(veb), Lo = shfl_up2(vob), Re = shfl_down2(vea), Ro = shfl_down2(voa);
+      // horizontal: fine col 4j (x_{c-1} + 6 x_c + x_{c+1}), 4j+1 (x_c + x_{c+1}), ...
+      float2 raw[8];
+      raw[0] = pfma(bc(6.f), vea, padd(Le, veb));
+      raw[1] = padd(vea, veb);
+      raw[2] = pfma(bc(6.f), veb, padd(vea, Re));
+      raw[3] = padd(veb, Re);
+      raw[4] = pfma(bc(6.f), voa, padd(Lo, vob));
+      raw[5] = padd(voa, vob);
+      raw[6] = pfma(bc(6.f), vob, padd(voa, Ro));
+      raw[7] = padd(vob, Ro);
+      const float2 w64 = P.cw[i][0], w16 = P.cw[i][1], w4 = P.cw[i][2];
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        const float2 w = (p < 4) ? ((p & 1) ? w16 : w64) : ((p & 1) ? w4 : w16);
+        float2 c = pfma(raw[p], w, pneg(bn[p]));
+        if (!LEVEL0) {
+          const float4 fv = fz[(p >> 2) * 2 + ((p & 3) >> 1)];
+          c = pfma((p & 1) ? hi2(fv) : lo2(fv), P.cw[i][3], c);
+        }
+        bn[p] = pfma(bc(tc[p]), bp[p], c);
+      }
+    };
+    auto stage_wait = [&]() -> const unsigned char* {
+      mbar_wait_parity(&full[s], ph);
+      return rowc + s * STAGE;
+    };
+    auto stage_release = [&]() {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (++s == S) {
+        s = 0;
+        ph ^= 1u;
+      }
+    };
+
+    int i = KL - 1;
+    if (OPS == 2) {
+#pragma unroll 1
+      for (; i >= 1; i -= 2) {
+        const unsigned char* so = stage_wait();
+        order(i, so, b2, b1);
+        order(i - 1, so + OBYTES, b1, b2);
+        stage_release();
+      }
+    } else {
+#pragma unroll 1
+      for (; i >= 1; i -= 2) {
+        order(i, stage_wait(), b2, b1);
+        stage_release();
+        order(i - 1, stage_wait(), b1, b2);
+        stage_release();
+      }
+    }
+    if (i == 0) {  // odd order count: the last b_k landed in b2
+      order(0, stage_wait(), b2, b1);
+      stage_release();
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        const float2 tmp = b1[p];
+        b1[p] = b2[p];
+        b2[p] = tmp;
+      }
+    }
+    // b1 = b_{k0}, b2 = b_{k0+1}
+    float res[8];
+    if (P.kbase == 1) {
+#pragma unroll
+      for (int p = 0; p < 8; ++p) res[p] = fmaf(b1[p].x, 0.5f * tc[p], fmaf(b1[p].y, sn[p], -b2[p].x));
+    } else {
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        float sk, ck;
+        sincos_turns_n(g[p], P.invT, P.kbase, &sk, &ck);
+        const float c1 = 0.5f * tc[p], s1 = sn[p];
+        const float cm = fmaf(ck, c1, sk * s1), sm = fmaf(sk, c1, -ck * s1);  // e^{i (k0-1) theta}
+        res[p] = fmaf(b1[p].x, ck, fmaf(b1[p].y, sk, -fmaf(b2[p].x, cm, b2[p].y * sm)));
+      }
+    }
+
+    // --- collapse: + up(D_{l+1}) from the tile header
+    if (HAS_D) {
+      float dq[3][2];
+      mbar_wait_parity(&dfull[hb], hph);
+      const int c0 = 60 * T.jb - 4;
+      const int cc0 = upmap(2 * j, P.Wc, P.Wf) - c0, cc1 = upmap(2 * j + 1, P.Wc, P.Wf) - c0;
+      const float* dh = reinterpret_cast<const float*>(hdr + HDR_D_OFF + warp * HDR_D_ROW);
+#pragma unroll
+      for (int tt = 0; tt < 3; ++tt) {
+        dq[tt][0] = dh[tt * (HDR_D_ROW / 4) + cc0];
+        dq[tt][1] = dh[tt * (HDR_D_ROW / 4) + cc1];
+      }
+      float hd[3][4];
+#pragma unroll
+      for (int tt = 0; tt < 3; ++tt) {
+        const float x0 = dq[tt][0], x1 = dq[tt][1];
+        const float L = __shfl_up_sync(FULL, x1, 1);
+        const float Rn = __shfl_down_sync(FULL, x0, 1);
+        hd[tt][0] = fmaf(6.f, x0, L + x1) * 0.125f;
+        hd[tt][1] = (x0 + x1) * 0.5f;
+        hd[tt][2] = fmaf(6.f, x1, x0 + Rn) * 0.125f;
+        hd[tt][3] = (x1 + Rn) * 0.5f;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        res[q] += 0.125f * fmaf(6.f, hd[1][q], hd[0][q] + hd[2][q]);
+        res[4 + q] += 0.5f * (hd[1][q] + hd[2][q]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&hempty[hb]);  // this warp is done with the tile header
+    if (LEVEL0 && P.include_base) {
+#pragma unroll
+      for (int p = 0; p < 8; ++p) res[p] += g[p];
+    }
+
+    if (act) {
+      const int xf0 = 4 * j;
+      const bool fvec_ok = xf0 + 3 < P.Wf;
+      float* op;
+      long long opitch;
+      bool oal;
+      if (LEVEL0) {
+        op = P.out + T.frame * P.out_fstride;
+        opitch = P.out_pitch;
+        oal = out_al;
+      } else {
+        op = P.fine.D + T.frame * P.fine.fstride_r;
+        opitch = P.fine.pitch;
+        oal = true;
+      }
+#pragma unroll
+      for (int tt = 0; tt < 2; ++tt) {
+        if (2 * r + tt >= P.Hf) break;
+        float* rp = op + (long long)(2 * r + tt) * opitch;
+        if (fvec_ok && oal) {
+          *reinterpret_cast<float4*>(rp + xf0) =
+              make_float4(res[4 * tt], res[4 * tt + 1], res[4 * tt + 2], res[4 * tt + 3]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (xf0 + q < P.Wf) rp[xf0 + q] = res[4 * tt + q];
+        }
+      }
+    }
+  }
+}
+
 template <typename Kern, typename... Args>
 cudaError_t launch_ex(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl, const Args&... args) {
   cudaLaunchConfig_t cfg = {};
@@ -829,6 +1409,19 @@ static cudaError_t launch_build_nc(BuildParams p, int batch, cudaStream_t s, boo
   return launch_ex(k_build<NC, 1, FROM_IMAGE, false>, grid, dim3(32), 0, s, pdl, p);
 }
 
+template <int NC>
+static cudaError_t launch_build0_nc(BuildParams p, int batch, cudaStream_t s, bool pdl) {
+  const int bx = (p.Wc + 29) / 30;
+  p.nchunks = p.KL / NC;
+  // strips of >= 4 output rows (the run loop needs R >= 2; halo rows 3/(2R))
+  int R = 16;
+  while (R > 4 && (long long)bx * ((p.Hc + R - 1) / R) * batch * p.nchunks < 148LL * 16) R >>= 1;
+  if (R > p.Hc) R = std::max(p.Hc, 2);
+  p.rows_per_strip = R;
+  dim3 grid(bx, (p.Hc + R - 1) / R, batch * p.nchunks);
+  return launch_ex(k_build0<NC>, grid, dim3(32), 0, s, pdl, p);
+}
+
 // largest channel chunk (<= cap) dividing the local order count
 static int chunk_for(int KL, int cap) {
   for (int c = cap; c > 1; --c)
@@ -845,6 +1438,27 @@ cudaError_t launch_build(const BuildParams& p0, int level_src, int batch, cudaSt
     dim3 grid(bx, (p.Hc + p.rows_per_strip - 1) / p.rows_per_strip, 1);
     if (level_src == 0) return launch_ex(k_build<0, 2, true, false>, grid, dim3(32), 0, s, pdl, p);
     return launch_ex(k_build<0, 2, false, false>, grid, dim3(32), 0, s, pdl, p);
+  }
+  static const bool b0v1 = [] {
+    const char* e = std::getenv("FLLF_BUILD0_V1");
+    return !(e && e[0] == '0');  // v2 opt-in (FLLF_BUILD0_V1=0) until verified on B200
+  }();
+  if (level_src == 0 && !b0v1) {
+    static const int cap = [] {
+      const char* e = std::getenv("FLLF_BUILD0V2_CHUNK");
+      const int v = e ? std::atoi(e) : 8;
+      return v >= 1 && v <= 8 ? v : 8;
+    }();
+    switch (chunk_for(p.KL, cap)) {
+      case 8: return launch_build0_nc<8>(p, batch, s, pdl);
+      case 7: return launch_build0_nc<7>(p, batch, s, pdl);
+      case 6: return launch_build0_nc<6>(p, batch, s, pdl);
+      case 5: return launch_build0_nc<5>(p, batch, s, pdl);
+      case 4: return launch_build0_nc<4>(p, batch, s, pdl);
+      case 3: return launch_build0_nc<3>(p, batch, s, pdl);
+      case 2: return launch_build0_nc<2>(p, batch, s, pdl);
+      default: return launch_build0_nc<1>(p, batch, s, pdl);
+    }
   }
   if (level_src == 0) {
     static const int cap0 = [] {
@@ -900,8 +1514,34 @@ static cudaError_t launch_apply_t(const ApplyParams& p, int batch, cudaStream_t 
   return launch_ex(k_apply<L0, HD, MP>, grid, dim3(160), smem, s, pdl, p, ntiles);
 }
 
+template <bool L0, bool HD>
+static cudaError_t launch_apply_cl_t(const ApplyParams& p, int batch, cudaStream_t s, bool pdl) {
+  const int ntiles = ((p.Wf + 119) / 120) * ((p.Hc + 3) / 4) * batch;
+  dim3 grid(std::min(ntiles, sm_count() * 3));
+  const int smem = apply_cl_smem<L0>();
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_apply_cl<L0, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  return launch_ex(k_apply_cl<L0, HD>, grid, dim3(160), smem, s, pdl, p, ntiles);
+}
+
 cudaError_t launch_apply(const ApplyParams& p, int level_fine, bool has_d, bool maps, int batch,
                          cudaStream_t s, bool pdl) {
+  static const bool v1 = [] {
+    const char* e = std::getenv("FLLF_APPLY_V1");
+    return e && e[0] == '1';
+  }();
+  if (!maps && !v1) {
+    if (level_fine == 0) {
+      if (has_d) return launch_apply_cl_t<true, true>(p, batch, s, pdl);
+      return launch_apply_cl_t<true, false>(p, batch, s, pdl);
+    }
+    if (has_d) return launch_apply_cl_t<false, true>(p, batch, s, pdl);
+    return launch_apply_cl_t<false, false>(p, batch, s, pdl);
+  }
 #define FLLF_APPLY(L0, HD, MP) return launch_apply_t<L0, HD, MP>(p, batch, s, pdl)
   if (level_fine == 0) {
     if (maps) {
