@@ -489,19 +489,36 @@ struct Build0Warp {
     Pr = Ar = make_float2(0.f, 0.f);
   }
 
-  // the two image pixels of fine row `row` (reflect-101)
-  __device__ __forceinline__ float2 load_row(int row) const {
-    const float* rp = isrc + (long long)refl101(row, P.Hf) * ipitch;
-    return EDGE ? make_float2(__ldg(rp + rc0), __ldg(rp + rc1)) : ldg2(rp + c0);
-  }
   struct Pair {
     float2 e, o;  // even / odd fine row, (col a, col b)
   };
-  // pair p holds rows 2(o0+p-1), 2(o0+p-1)+1 (p = 0: the two halo rows above)
-  __device__ __forceinline__ void load_pair(int p, Pair& d) const {
+  // I rows are staged through a per-warp shared-memory ring with cp.async:
+  // PD row pairs in flight without holding them in registers.
+  static constexpr int PD = 8;
+  float2 (*ring)[2][32];
+  // issue the copies of pair p (rows 2(o0+p-1), +1; p = 0: the two halo rows above)
+  __device__ __forceinline__ void issue_pair(int p) const {
+    const int lane = threadIdx.x & 31;
     const int r0 = 2 * (o0 + p - 1);
-    d.e = load_row(r0);
-    d.o = load_row(r0 + 1);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float* rp = isrc + (long long)refl101(r0 + h, P.Hf) * ipitch;
+      float2* d = &ring[p % PD][h][lane];
+      if (EDGE) {
+        cp_async4(&d->x, rp + rc0);
+        cp_async4(&d->y, rp + rc1);
+      } else {
+        cp_async8(d, rp + c0);
+      }
+    }
+    cp_async_commit();
+  }
+  __device__ __forceinline__ Pair read_pair(int p) const {
+    const int lane = threadIdx.x & 31;
+    Pair d;
+    d.e = ring[p % PD][0][lane];
+    d.o = ring[p % PD][1][lane];
+    return d;
   }
 
   // horizontal [1,4,6,4,1] + decimation of a finished row (complex), a = col 2x, b = 2x+1
@@ -581,35 +598,31 @@ struct Build0Warp {
   }
 
   // Stream the strip: pairs 0 (halo rows) .. R and the final row (even row of
-  // pair R+1); two pairs per iteration with static buffers (the next two
-  // pairs are in flight while one is processed).
+  // pair R+1), PD pairs in flight through the shared-memory ring.
   __device__ __forceinline__ void run(int R) {
-    Pair BA, BB;
-    load_pair(0, BA);
-    load_pair(1, BB);
-    proc<false, false>(BA, 0);
-    load_pair(2, BA);
-    proc<false, false>(BB, 0);
-    load_pair(3, BB);
-    int p = 2;
+#pragma unroll
+    for (int q = 0; q < PD; ++q) issue_pair(q);
+    cp_async_wait<PD - 1>();
+    proc<false, false>(read_pair(0), 0);
+    issue_pair(PD);
+    cp_async_wait<PD - 1>();
+    proc<false, false>(read_pair(1), 0);
+    issue_pair(PD + 1);
 #pragma unroll 1
-    for (; p + 1 <= R; p += 2) {
-      proc<true, false>(BA, o0 + p - 2);
-      load_pair(p + 2, BA);
-      proc<true, false>(BB, o0 + p - 1);
-      load_pair(p + 3, BB);
+    for (int p = 2; p <= R; ++p) {
+      cp_async_wait<PD - 1>();
+      const Pair d = read_pair(p);
+      issue_pair(p + PD);  // beyond the strip: harmless reflected reads
+      proc<true, false>(d, o0 + p - 2);
     }
-    if (p <= R) {
-      proc<true, false>(BA, o0 + p - 2);
-      proc<true, true>(BB, o0 + R - 1);
-    } else {
-      proc<true, true>(BA, o0 + R - 1);
-    }
+    cp_async_wait<PD - 1>();
+    proc<true, true>(read_pair(R + 1), o0 + R - 1);
+    cp_async_wait<0>();
   }
 };
 
 template <int NC>
-__global__ void __launch_bounds__(32) k_build0(const BuildParams P) {
+__global__ void __launch_bounds__(32, 16) k_build0(const BuildParams P) {
   pdl_trigger();
   const int cb = blockIdx.x;
   if (cb * 30 >= P.Wc) return;
@@ -621,11 +634,14 @@ __global__ void __launch_bounds__(32) k_build0(const BuildParams P) {
   const int frame = blockIdx.z % nframes;
   bool interior = (60 * cb - 2 >= 0) && (60 * cb + 61 < P.Wf);
   interior = interior && ((reinterpret_cast<uintptr_t>(P.img.p) & 7) == 0) && ((P.img.pitch & 1) == 0);
+  __shared__ __align__(16) float2 ring[Build0Warp<NC, false>::PD][2][32];
   if (interior) {
     Build0Warp<NC, false> w(P, cb, o0, chunk, frame);
+    w.ring = ring;
     w.run(R);
   } else {
     Build0Warp<NC, true> w(P, cb, o0, chunk, frame);
+    w.ring = ring;
     w.run(R);
   }
 }
@@ -1441,7 +1457,7 @@ cudaError_t launch_build(const BuildParams& p0, int level_src, int batch, cudaSt
   }
   static const bool b0v1 = [] {
     const char* e = std::getenv("FLLF_BUILD0_V1");
-    return !(e && e[0] == '0');  // v2 opt-in (FLLF_BUILD0_V1=0) until verified on B200
+    return e && e[0] == '1';  // FLLF_BUILD0_V1=1: the previous level-0 build (A/B only)
   }();
   if (level_src == 0 && !b0v1) {
     static const int cap = [] {

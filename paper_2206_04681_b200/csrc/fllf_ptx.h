@@ -88,6 +88,21 @@ __device__ __forceinline__ bool elect_one() {
   return pred != 0;
 }
 
+// cp.async (LDGSTS): per-thread global -> shared copies of 4 / 8 bytes, grouped
+// with commit / wait_group (each thread reads back only what it copied itself,
+// so no barrier is needed after the wait).
+__device__ __forceinline__ void cp_async4(void* dst_smem, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst_smem)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst_smem, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst_smem)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // Programmatic dependent launch (PDL).  wait: block until the preceding
 // grid in the stream has completed and its writes are visible (no-op when the
 // kernel was not launched with programmatic stream serialization);
