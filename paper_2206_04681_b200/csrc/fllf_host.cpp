@@ -1,5 +1,7 @@
 // libfllf C ABI: plan creation, workspace layout, fp64 coefficient math and
 // launch sequencing (DESIGN.md "Boundary" and "Data layout in HBM").
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -88,9 +90,43 @@ struct fllf_plan_s {
   bool g_prof = false;
   int g_launches = 0;
   int g_nrec = 0;
+  // TMA descriptors of each level's Z planes (k_apply_cl): as the coarse
+  // level (box 128 floats x 6 rows) and as the fine level (box 256 x 8)
+  bool tm_ok = false;
+  CUtensorMap tmc[FLLF_MAX_LEVELS];
+  CUtensorMap tmf[FLLF_MAX_LEVELS];
 };
 
 namespace {
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    cudaGetLastError();
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+// Z planes of one level as a 3-D fp32 tensor: (2 * zpitch floats) x H rows x
+// (batch * KL) planes; box (bx floats, by rows, 1 plane).
+bool encode_z_map(CUtensorMap* m, const fllf::DevLevel& L, int planes, unsigned bx, unsigned by) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  void* base = const_cast<float2*>(L.Z - fllf::ZHALO);
+  const cuuint64_t dims[3] = {(cuuint64_t)(2 * L.zpitch), (cuuint64_t)L.H, (cuuint64_t)planes};
+  const cuuint64_t strides[2] = {(cuuint64_t)L.zpitch * 8, (cuuint64_t)L.kstride_z * 8};
+  const cuuint32_t box[3] = {bx, by, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // Bracket one launch with profiling events (no-op when profiling is off).
 struct ProfScope {
   fllf_plan p;
@@ -295,6 +331,15 @@ fllf_status fllf_plan_create_ex(const fllf_plan_desc* din, fllf_plan* out) {
     p->lv[l].G = reinterpret_cast<float*>(base + offG[l]);
     p->lv[l].D = reinterpret_cast<float*>(base + offD[l]);
     p->lv[l].Z = reinterpret_cast<float2*>(base + offZ[l]) + fllf::ZHALO;
+  }
+  {
+    bool ok = true;
+    for (int l = 1; l < d.levels && ok; ++l) {
+      ok = encode_z_map(&p->tmc[l], p->lv[l], (int)B * p->KL, 128, 6) &&
+           encode_z_map(&p->tmf[l], p->lv[l], (int)B * p->KL, 256, 8);
+    }
+    const char* nt = std::getenv("FLLF_NO_TENSOR_TMA");
+    p->tm_ok = ok && !(nt && nt[0] == '1');
   }
   // halo / padding cells that no kernel writes must hold finite values
   e = cudaMemset(p->ws, 0, off);
@@ -504,6 +549,11 @@ fllf_status fllf_apply(fllf_plan p, const fllf_apply_args* a, float* d_out, size
   for (int l = lmax - 1; l >= 0; --l) {
     if (l > 0) ap.fine = p->lv[l];
     ap.coarse = p->lv[l + 1];
+    ap.use_tm = p->tm_ok ? 1 : 0;
+    if (p->tm_ok) {
+      ap.tm_coarse = p->tmc[l + 1];
+      if (l > 0) ap.tm_fine = p->tmf[l];
+    }
     ap.Hf = p->Hs[l];
     ap.Wf = p->Ws[l];
     ap.Hc = p->Hs[l + 1];

@@ -1,6 +1,7 @@
 // Internal structures shared by the host code (fllf_host.cpp) and the kernels
 // (fllf_kernels.cu).  Not part of the C ABI.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -57,6 +58,13 @@ struct BuildParams {
 };
 
 struct ApplyParams {
+  // TMA tensor maps (3-D: float columns x rows x (frame, order) planes) of the
+  // coarse level's Z planes (box 128 floats x 6 rows) and the fine level's
+  // (box 256 x 8): one tensor copy per order stage for interior tiles
+  // (k_apply_cl); use_tm = 0 -> per-row bulk copies only.
+  CUtensorMap tm_coarse;
+  CUtensorMap tm_fine;
+  int use_tm;
   DevImage img;        // level-0 input image I (LEVEL0 kernels)
   float* out;          // level-0 output O (LEVEL0 kernels)
   long long out_pitch; // floats

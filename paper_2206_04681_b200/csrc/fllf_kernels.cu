@@ -1044,7 +1044,7 @@ __host__ __device__ constexpr int apply_cl_smem() {
 }
 
 template <bool LEVEL0, bool HAS_D>
-__global__ void __launch_bounds__(160, 3) k_apply_cl(const ApplyParams P, const int ntiles) {
+__global__ void __launch_bounds__(160, 3) k_apply_cl(const __grid_constant__ ApplyParams P, const int ntiles) {
   constexpr int S = apply_cl_stages<LEVEL0>();
   constexpr int OPS = apply_cl_ops<LEVEL0>();
   constexpr int OBYTES = apply_stage_bytes<LEVEL0>();  // one order
@@ -1125,6 +1125,10 @@ __global__ void __launch_bounds__(160, 3) k_apply_cl(const ApplyParams P, const 
 #pragma unroll
       for (int q = 0; q < 6; ++q) crow[q] = upmap(T.r0 - 1 + q, P.Hc, P.Hf);
       const float2* zf0 = LEVEL0 ? nullptr : P.fine.Z + T.frame * P.fine.fstride_z + (120 * T.jb - 4);
+      // interior tiles: the 6 coarse (8 fine) rows are contiguous -> one tensor copy per order
+      const bool tmc = P.use_tm && T.r0 >= 1 && T.r0 + 4 <= P.Hc - 1;
+      const bool tmf = !LEVEL0 && P.use_tm && 2 * T.r0 + 7 <= P.Hf - 1;
+      const int xc = 2 * (ZHALO + 60 * T.jb - 2), xf = 2 * (ZHALO + 120 * T.jb - 4);  // float columns
 #pragma unroll 1
       for (int i = KL - 1; i >= 0; i -= OPS) {
         if (n >= S) mbar_wait_parity(&empty[s], ph ^ 1u);
@@ -1135,17 +1139,25 @@ __global__ void __launch_bounds__(160, 3) k_apply_cl(const ApplyParams P, const 
 #pragma unroll
           for (int h = 0; h < OPS; ++h) {
             if (h < no) {
-              const float2* zc = zc0 + (long long)(i - h) * P.coarse.kstride_z;
               unsigned char* so = st + h * OBYTES;
+              if (tmc) {
+                tma_load_3d(so, &P.tm_coarse, xc, T.r0 - 1, T.frame * KL + i - h, &full[s]);
+              } else {
+                const float2* zc = zc0 + (long long)(i - h) * P.coarse.kstride_z;
 #pragma unroll
-              for (int q = 0; q < 6; ++q)
-                tma_load_1d(so + q * CROW_BYTES, zc + (long long)crow[q] * P.coarse.zpitch, CROW_BYTES, &full[s]);
+                for (int q = 0; q < 6; ++q)
+                  tma_load_1d(so + q * CROW_BYTES, zc + (long long)crow[q] * P.coarse.zpitch, CROW_BYTES, &full[s]);
+              }
               if (!LEVEL0) {
-                const float2* zf = zf0 + (long long)(i - h) * P.fine.kstride_z;
+                if (tmf) {
+                  tma_load_3d(so + FOFF, &P.tm_fine, xf, 2 * T.r0, T.frame * KL + i - h, &full[s]);
+                } else {
+                  const float2* zf = zf0 + (long long)(i - h) * P.fine.kstride_z;
 #pragma unroll
-                for (int q = 0; q < 8; ++q)
-                  tma_load_1d(so + FOFF + q * FROW_BYTES,
-                              zf + (long long)min(2 * T.r0 + q, P.Hf - 1) * P.fine.zpitch, FROW_BYTES, &full[s]);
+                  for (int q = 0; q < 8; ++q)
+                    tma_load_1d(so + FOFF + q * FROW_BYTES,
+                                zf + (long long)min(2 * T.r0 + q, P.Hf - 1) * P.fine.zpitch, FROW_BYTES, &full[s]);
+                }
               }
             }
           }

@@ -49,6 +49,18 @@ __device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src_gmem
       : "memory");
 }
 
+// 3-D tensor copy global -> shared through a TMA descriptor (a __grid_constant__
+// kernel parameter); coordinates are element indices, innermost first;
+// out-of-bounds elements are zero-filled and still count as transaction bytes.
+__device__ __forceinline__ void tma_load_3d(void* dst_smem, const void* tmap, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(smem_u32(dst_smem)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // Warp-wide variants for a producer warp whose control flow and operands are
 // warp-uniform: one elected lane issues (the operands then stay in uniform
 // registers; a lane-0 branch would make ptxas wrap every copy in a
