@@ -573,7 +573,7 @@ struct Build0Warp {
         const float2 ea = padd(Pc[i][0], zc[0]);
         const float2 eb = padd(Pc[i][1], zc[1]);
         const float2 h = hsum_c(ea, eb);
-        float2* q = zdst + (off0 + i * (int)P.dst.kstride_z);
+        float2* q = zdst + (unsigned)(off0 + i * (int)P.dst.kstride_z);  // IMAD.WIDE.U32
         if (store_lane) q[0] = h;
         if (EDGE) {
           if (halo_l) q[-2] = h;  // x == 1: column -1
@@ -678,6 +678,37 @@ __device__ __forceinline__ ApplyTile apply_tile(int t, const ApplyParams& P) {
   T.frame = t / ny;
   return T;
 }
+
+// Tile sequence t = blockIdx.x, blockIdx.x + gridDim.x, ... decomposed
+// incrementally (no divisions per tile).
+struct TileIter {
+  int nx, ny, dj, dr, df;
+  ApplyTile T;
+  __device__ __forceinline__ TileIter(const ApplyParams& P) {
+    nx = (P.Wf + 119) / 120;
+    ny = (P.Hc + 3) / 4;
+    const int q = gridDim.x / nx;
+    dj = gridDim.x - q * nx;
+    dr = q % ny;
+    df = q / ny;
+    T = apply_tile(blockIdx.x, P);
+    T.r0 >>= 2;  // row block index while iterating
+  }
+  __device__ __forceinline__ ApplyTile tile() const {
+    ApplyTile u = T;
+    u.r0 *= 4;
+    return u;
+  }
+  __device__ __forceinline__ void next() {
+    T.jb += dj;
+    int c = T.jb >= nx;
+    T.jb -= c ? nx : 0;
+    T.r0 += dr + c;
+    c = T.r0 >= ny;
+    T.r0 -= c ? ny : 0;
+    T.frame += df + c;
+  }
+};
 
 template <bool LEVEL0, bool HAS_D, bool MAPS>
 __global__ void __launch_bounds__(160, MAPS ? 2 : 3) k_apply(const ApplyParams P, const int ntiles) {
@@ -1092,8 +1123,9 @@ __global__ void __launch_bounds__(160, 3) k_apply_cl(const __grid_constant__ App
     uint32_t ph = 0;
     int n = 0, nt = 0;
     bool waited = P.wait_first != 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
-      const ApplyTile T = apply_tile(t, P);
+    TileIter it(P);
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt, it.next()) {
+      const ApplyTile T = it.tile();
       const int hb = nt & 1;
       unsigned char* hdr = smem + HOFF + hb * HDR_BYTES;
       if (nt >= 2) mbar_wait_parity(&hempty[hb], ((nt >> 1) & 1) ^ 1u);
@@ -1196,9 +1228,10 @@ __global__ void __launch_bounds__(160, 3) k_apply_cl(const __grid_constant__ App
   int s = 0;
   uint32_t ph = 0;
   int nt = 0;
+  TileIter it(P);
 #pragma unroll 1
-  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt) {
-    const ApplyTile T = apply_tile(t, P);
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt, it.next()) {
+    const ApplyTile T = it.tile();
     const int hb = nt & 1;
     const uint32_t hph = (nt >> 1) & 1;
     const unsigned char* hdr = smem + HOFF + hb * HDR_BYTES;
