@@ -497,18 +497,37 @@ struct Build0Warp {
   static constexpr int PD = 8;
   float2 (*ring)[2][32];
   // issue the copies of pair p (rows 2(o0+p-1), +1; p = 0: the two halo rows above)
-  __device__ __forceinline__ void issue_pair(int p) const {
+  // rows_in: no row of this strip's reads (incl. the prefetch overrun) needs
+  // reflection -> the row pointer just advances by two rows per pair
+  bool rows_in;
+  const float* rowp;  // this lane's column in fine row 2(o0+p-1) of the next pair to issue
+  __device__ __forceinline__ void issue_pair(int p) {
     const int lane = threadIdx.x & 31;
-    const int r0 = 2 * (o0 + p - 1);
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const float* rp = isrc + (long long)refl101(r0 + h, P.Hf) * ipitch;
-      float2* d = &ring[p % PD][h][lane];
+    float2* d0 = &ring[p % PD][0][lane];
+    float2* d1 = &ring[p % PD][1][lane];
+    if (rows_in) {
       if (EDGE) {
-        cp_async4(&d->x, rp + rc0);
-        cp_async4(&d->y, rp + rc1);
+        cp_async4(&d0->x, rowp + rc0);
+        cp_async4(&d0->y, rowp + rc1);
+        cp_async4(&d1->x, rowp + ipitch + rc0);
+        cp_async4(&d1->y, rowp + ipitch + rc1);
       } else {
-        cp_async8(d, rp + c0);
+        cp_async8(d0, rowp + c0);
+        cp_async8(d1, rowp + ipitch + c0);
+      }
+      rowp += 2 * ipitch;
+    } else {
+      const int r0 = 2 * (o0 + p - 1);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float* rp = isrc + (long long)refl101(r0 + h, P.Hf) * ipitch;
+        float2* d = h ? d1 : d0;
+        if (EDGE) {
+          cp_async4(&d->x, rp + rc0);
+          cp_async4(&d->y, rp + rc1);
+        } else {
+          cp_async8(d, rp + c0);
+        }
       }
     }
     cp_async_commit();
@@ -600,6 +619,9 @@ struct Build0Warp {
   // Stream the strip: pairs 0 (halo rows) .. R and the final row (even row of
   // pair R+1), PD pairs in flight through the shared-memory ring.
   __device__ __forceinline__ void run(int R) {
+    // pairs 0 .. R+1+PD are read: rows 2(o0-1) .. 2(o0+R+PD)+1
+    rows_in = o0 >= 1 && 2 * (o0 + R + PD) + 1 < P.Hf;
+    rowp = isrc + (long long)(2 * (o0 - 1)) * ipitch;
 #pragma unroll
     for (int q = 0; q < PD; ++q) issue_pair(q);
     cp_async_wait<PD - 1>();
@@ -1476,7 +1498,8 @@ static cudaError_t launch_build0_nc(BuildParams p, int batch, cudaStream_t s, bo
   p.nchunks = p.KL / NC;
   // strips of >= 4 output rows (the run loop needs R >= 2; halo rows 3/(2R))
   int R = 16;
-  while (R > 4 && (long long)bx * ((p.Hc + R - 1) / R) * batch * p.nchunks < 148LL * 16) R >>= 1;
+  { const char* e = std::getenv("FLLF_B0_WARPS"); const long long tw = e ? std::atoll(e) : 148LL * 8;
+    while (R > 4 && (long long)bx * ((p.Hc + R - 1) / R) * batch * p.nchunks < tw) R >>= 1; }
   if (R > p.Hc) R = std::max(p.Hc, 2);
   p.rows_per_strip = R;
   dim3 grid(bx, (p.Hc + R - 1) / R, batch * p.nchunks);
