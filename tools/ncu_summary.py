@@ -1,6 +1,11 @@
 """Summarise an ncu report (--set full) into markdown + roofline traffic json.
 
-    python tools/ncu_summary.py gpurun_out/prof.ncu-rep profiles/r01_ncu_full.md [workload]
+    python tools/ncu_summary.py gpurun_out/prof.ncu-rep profiles/r01_ncu_full.md [workload [levels]]
+
+With `levels`, the launches are taken as one filter sequence (build0,
+build 1..levels-2, apply levels-2..1, apply0) and their DRAM read+write bytes
+are merged into profiles/roofline_traffic.json under "<workload>:<kind>:<level>"
+(read by bench.py for the roofline `traffic` field).
 """
 import csv
 import io
@@ -57,3 +62,25 @@ md = [f"# ncu --set full summary: `{os.path.basename(rep)}` ({workload})", "",
       "Per launch, cold caches (ncu replays each kernel with caches flushed), --clock-control none.", ""] + lines
 open(out_md, "w").write("\n".join(md) + "\n")
 print("\n".join(md))
+if len(sys.argv) > 4:
+    levels = int(sys.argv[4])
+    order = [("build0", 0)] + [("build", l) for l in range(1, levels - 1)] + \
+            [("apply", l) for l in range(levels - 2, 0, -1)] + [("apply0", 0)]
+    vals = [v for k in seen for v in seen[k]]
+    # launches in report order
+    rows_bytes = []
+    for r in data:
+        def mbv(k):
+            v = float(g(r, k) or 0)
+            u = units[hdr.index(k)] if k in hdr else "byte"
+            return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
+        rows_bytes.append(mbv("dram__bytes_read.sum") + mbv("dram__bytes_write.sum"))
+    if len(rows_bytes) >= len(order):
+        tp = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
+                          "roofline_traffic.json")
+        tj = json.load(open(tp)) if os.path.exists(tp) else {}
+        for (kind, lev), b in zip(order, rows_bytes[:len(order)]):
+            tj[f"{workload}:{kind}:{lev}"] = round(b)
+        json.dump(tj, open(tp, "w"), indent=1, sort_keys=True)
+        print("traffic ->", tp)
+
