@@ -155,6 +155,47 @@ FLLF_API fllf_status fllf_coefficients(int K, double T, double sigma_r, double m
  * P:296). */
 FLLF_API fllf_status fllf_optimal_period(int K, double sigma_r, double R, double* T_out);
 
+/* ---- Colour + variance-driven gain (Sec. IV, P:373-377:
+ * "The degree of enhancement is determined according to the variance of the
+ * pixels in a local window; the low variance is a small enhancement" and
+ * "LLF is applied to the Y channel of the YUV color space, and the other
+ * components are kept"; Sec. III-B, per-pixel m_p).  Readings
+ * (R13-R16): YUV = BT.601 full-range YCbCr with zero-centred
+ * chroma; local variance = population variance over the (2r+1)^2 window,
+ * reflect-101 borders; m_p = m_lo + (m_hi - m_lo) min(1, v_p / v_ref);
+ * sigma_r uniform (the plan's).
+ *
+ * Planar colour images: plane c of a 3-plane image lives at
+ * (char*)base + c*H*pitch_bytes; rows as for grayscale images. */
+#define FLLF_MAX_GAIN_RADIUS 32
+
+typedef struct {
+  int radius;      /* window half-size r, 0 <= r <= FLLF_MAX_GAIN_RADIUS          */
+  double m_lo;     /* gain at zero variance (flat regions)                         */
+  double m_hi;     /* gain at v_p >= v_ref                                         */
+  double v_ref;    /* variance at which the gain saturates, > 0                    */
+} fllf_gain_desc;
+
+/* d_rgb -> d_yuv (3 planes each, device, same pitch; may not alias).
+ * INVALID_ARGUMENT: H, W < 1.  BAD_POINTER: NULL or bad pitch. */
+FLLF_API fllf_status fllf_rgb_to_yuv(const float* d_rgb, float* d_yuv, int H, int W, size_t pitch_bytes,
+                                     void* s);
+/* Inverse of fllf_rgb_to_yuv. */
+FLLF_API fllf_status fllf_yuv_to_rgb(const float* d_yuv, float* d_rgb, int H, int W, size_t pitch_bytes,
+                                     void* s);
+/* Gain map m_p from the local variance of d_y (H x W, device) into d_m.
+ * INVALID_ARGUMENT: bad sizes, radius out of range, v_ref <= 0, non-finite. */
+FLLF_API fllf_status fllf_gain_map(const float* d_y, size_t y_pitch_bytes, int H, int W,
+                                   const fllf_gain_desc* g, float* d_m, size_t m_pitch_bytes, void* s);
+/* The Fig. 5 pipeline on a plan with batch 1: RGB -> YUV, build the pyramids
+ * of Y, gain map, apply(FLLF_MAPS) with sigma_r = the plan's and m = the gain
+ * map, U and V kept, YUV -> RGB into d_rgb_out.  Workspace for the YUV
+ * planes and maps is owned by the plan (allocated on first use).  d_rgb and
+ * d_rgb_out may not alias.  INVALID_ARGUMENT: plan batch != 1 or a bad
+ * gain description. */
+FLLF_API fllf_status fllf_enhance_rgb(fllf_plan p, const float* d_rgb, float* d_rgb_out, size_t pitch_bytes,
+                                      const fllf_gain_desc* g, void* s);
+
 /* Introspection (tests, tooling). */
 FLLF_API fllf_status fllf_plan_level_dims(fllf_plan p, int level, int* H, int* W);
 FLLF_API fllf_status fllf_workspace_bytes(fllf_plan p, size_t* bytes);

@@ -70,6 +70,9 @@ struct fllf_plan_s {
   long long img_pitch = 0;     // floats
   float* stage_in = nullptr;
   float* stage_out = nullptr;
+  // fllf_enhance_rgb workspace: Y, U, V, Y', sigma map, m map (H x W each, pitch W)
+  float* color_ws = nullptr;
+  float color_sigma = -1.f;  // sigma value the sigma map currently holds
   int last_launches = 0;
   // profiling: one (start, stop) event pair per launch record
   bool profiling = false;
@@ -360,6 +363,7 @@ fllf_status fllf_destroy(fllf_plan p) {
     if (p->ws) cudaFree(p->ws);
     if (p->maps_ws) cudaFree(p->maps_ws);
     if (p->stage_in) cudaFree(p->stage_in);
+    if (p->color_ws) cudaFree(p->color_ws);
     if (p->stage_out) cudaFree(p->stage_out);
     for (cudaEvent_t e : p->ev_start) cudaEventDestroy(e);
     for (cudaEvent_t e : p->ev_stop) cudaEventDestroy(e);
@@ -654,6 +658,138 @@ fllf_status fllf_filter_host(fllf_plan p, const float* h_img, float* h_out, void
   if (st != FLLF_OK) return st;
   e = cudaMemcpyAsync(h_out, p->stage_out, bytes, cudaMemcpyDeviceToHost, stream);
   if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
+  return FLLF_OK;
+}
+
+// ---------------------------------------------------------------- NEXT-3
+static fllf_status color_common(const float* a, const float* b, int H, int W, size_t pitch_bytes,
+                                long long* pitch) {
+  if (H < 1 || W < 1) return fail(FLLF_ERR_INVALID_ARGUMENT, "colour: H and W must be >= 1");
+  fllf_status st = check_image(a, pitch_bytes, W, "colour: input", pitch);
+  if (st != FLLF_OK) return st;
+  st = check_image(b, pitch_bytes, W, "colour: output", pitch);
+  if (st != FLLF_OK) return st;
+  if (a == b) return fail(FLLF_ERR_BAD_POINTER, "colour: input and output may not alias");
+  return FLLF_OK;
+}
+
+static fllf::ColorParams color_params(const float* src, float* dst, int H, int W, long long pitch) {
+  fllf::ColorParams c{};
+  for (int i = 0; i < 3; ++i) {
+    c.src[i] = src + (long long)i * H * pitch;
+    c.dst[i] = dst + (long long)i * H * pitch;
+  }
+  c.H = H;
+  c.W = W;
+  c.pitch = pitch;
+  return c;
+}
+
+fllf_status fllf_rgb_to_yuv(const float* d_rgb, float* d_yuv, int H, int W, size_t pitch_bytes, void* s) {
+  long long pitch;
+  fllf_status st = color_common(d_rgb, d_yuv, H, W, pitch_bytes, &pitch);
+  if (st != FLLF_OK) return st;
+  cudaError_t e = fllf::launch_rgb_to_yuv(color_params(d_rgb, d_yuv, H, W, pitch), static_cast<cudaStream_t>(s));
+  return e == cudaSuccess ? FLLF_OK : cuda_fail(e, "rgb_to_yuv launch");
+}
+
+fllf_status fllf_yuv_to_rgb(const float* d_yuv, float* d_rgb, int H, int W, size_t pitch_bytes, void* s) {
+  long long pitch;
+  fllf_status st = color_common(d_yuv, d_rgb, H, W, pitch_bytes, &pitch);
+  if (st != FLLF_OK) return st;
+  cudaError_t e = fllf::launch_yuv_to_rgb(color_params(d_yuv, d_rgb, H, W, pitch), static_cast<cudaStream_t>(s));
+  return e == cudaSuccess ? FLLF_OK : cuda_fail(e, "yuv_to_rgb launch");
+}
+
+static fllf_status check_gain(const fllf_gain_desc* g) {
+  if (!g) return fail(FLLF_ERR_BAD_POINTER, "gain: NULL description");
+  if (g->radius < 0 || g->radius > FLLF_MAX_GAIN_RADIUS)
+    return fail(FLLF_ERR_INVALID_ARGUMENT, "gain: radius must be in 0..FLLF_MAX_GAIN_RADIUS");
+  if (!is_finite(g->m_lo) || !is_finite(g->m_hi) || !is_finite(g->v_ref) || !(g->v_ref > 0))
+    return fail(FLLF_ERR_INVALID_ARGUMENT, "gain: m_lo, m_hi finite and v_ref > 0 required");
+  return FLLF_OK;
+}
+
+fllf_status fllf_gain_map(const float* d_y, size_t y_pitch_bytes, int H, int W, const fllf_gain_desc* g,
+                          float* d_m, size_t m_pitch_bytes, void* s) {
+  if (H < 1 || W < 1) return fail(FLLF_ERR_INVALID_ARGUMENT, "gain: H and W must be >= 1");
+  fllf_status st = check_gain(g);
+  if (st != FLLF_OK) return st;
+  long long yp, mp;
+  st = check_image(d_y, y_pitch_bytes, W, "gain: d_y", &yp);
+  if (st != FLLF_OK) return st;
+  st = check_image(d_m, m_pitch_bytes, W, "gain: d_m", &mp);
+  if (st != FLLF_OK) return st;
+  fllf::GainParams gp{};
+  gp.y = d_y;
+  gp.y_pitch = yp;
+  gp.m = d_m;
+  gp.m_pitch = mp;
+  gp.H = H;
+  gp.W = W;
+  gp.radius = g->radius;
+  gp.m_lo = g->m_lo;
+  gp.m_hi = g->m_hi;
+  gp.inv_vref = 1.0 / g->v_ref;
+  cudaError_t e = fllf::launch_gain_map(gp, static_cast<cudaStream_t>(s));
+  return e == cudaSuccess ? FLLF_OK : cuda_fail(e, "gain_map launch");
+}
+
+fllf_status fllf_enhance_rgb(fllf_plan p, const float* d_rgb, float* d_rgb_out, size_t pitch_bytes,
+                             const fllf_gain_desc* g, void* s) {
+  if (!p) return fail(FLLF_ERR_BAD_POINTER, "NULL plan");
+  if (p->d.batch != 1) return fail(FLLF_ERR_INVALID_ARGUMENT, "enhance_rgb: plan batch must be 1");
+  fllf_status st = check_gain(g);
+  if (st != FLLF_OK) return st;
+  const int H = p->d.H, W = p->d.W;
+  long long pitch;
+  st = color_common(d_rgb, d_rgb_out, H, W, pitch_bytes, &pitch);
+  if (st != FLLF_OK) return st;
+  if (pitch != W) return fail(FLLF_ERR_BAD_POINTER, "enhance_rgb: planes must be dense (pitch_bytes 0 or W*4)");
+  DeviceGuard guard(p->device);
+  cudaStream_t stream = static_cast<cudaStream_t>(s);
+  const size_t plane = (size_t)H * W;
+  if (!p->color_ws) {
+    if (cudaMalloc(&p->color_ws, 6 * plane * sizeof(float)) != cudaSuccess) {
+      cudaGetLastError();
+      p->color_ws = nullptr;
+      return fail(FLLF_ERR_OUT_OF_MEMORY, "enhance_rgb workspace cudaMalloc failed");
+    }
+    p->color_sigma = -1.f;
+  }
+  float* yuv = p->color_ws;             // Y, U, V
+  float* yo = p->color_ws + 3 * plane;  // Y' (the LLF output)
+  float* smap = p->color_ws + 4 * plane;
+  float* mmap = p->color_ws + 5 * plane;
+  cudaError_t e = fllf::launch_rgb_to_yuv(color_params(d_rgb, yuv, H, W, pitch), stream);
+  if (e != cudaSuccess) return cuda_fail(e, "rgb_to_yuv launch");
+  st = fllf_build_fourier_pyramids(p, yuv, 0, s);
+  if (st != FLLF_OK) return st;
+  st = fllf_gain_map(yuv, 0, H, W, g, mmap, 0, s);
+  if (st != FLLF_OK) return st;
+  const float sig = (float)p->d.sigma_r;
+  if (p->color_sigma != sig) {  // the uniform sigma_r map (R16), filled once per plan
+    e = fllf::launch_fill(smap, W, H, W, sig, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "sigma map fill");
+    p->color_sigma = sig;
+  }
+  fllf_apply_args a{};
+  a.mode = FLLF_MAPS;
+  a.d_sigma_r = smap;
+  a.d_m = mmap;
+  a.map_pitch_bytes = 0;
+  st = fllf_apply(p, &a, yo, 0, s);
+  if (st != FLLF_OK) return st;
+  fllf::ColorParams c{};
+  c.src[0] = yo;
+  c.src[1] = yuv + plane;
+  c.src[2] = yuv + 2 * plane;
+  for (int i = 0; i < 3; ++i) c.dst[i] = d_rgb_out + (long long)i * H * pitch;
+  c.H = H;
+  c.W = W;
+  c.pitch = pitch;
+  e = fllf::launch_yuv_to_rgb(c, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "yuv_to_rgb launch");
   return FLLF_OK;
 }
 

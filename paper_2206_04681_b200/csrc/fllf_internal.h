@@ -93,6 +93,30 @@ struct ApplyParams {
   float2 cw[FLLF_MAX_K][4];
 };
 
+// Colour conversion (fllf_color.cu): three planes in, three planes out, all
+// with the same row pitch (floats).
+struct ColorParams {
+  const float* src[3];
+  float* dst[3];
+  int H, W;
+  long long pitch;
+};
+
+// Variance-driven gain map (fllf_color.cu).
+struct GainParams {
+  const float* y;
+  long long y_pitch;
+  float* m;
+  long long m_pitch;
+  int H, W, radius;
+  double m_lo, m_hi, inv_vref;
+};
+
+cudaError_t launch_rgb_to_yuv(const ColorParams& p, cudaStream_t s);
+cudaError_t launch_yuv_to_rgb(const ColorParams& p, cudaStream_t s);
+cudaError_t launch_gain_map(const GainParams& p, cudaStream_t s);
+cudaError_t launch_fill(float* ptr, long long pitch, int H, int W, float v, cudaStream_t s);
+
 // Kernel launchers (fllf_kernels.cu).  Return cudaGetLastError() after launch.
 // pdl: launch with programmatic stream serialization (the kernel may start
 // while its predecessor is still running; it synchronises with griddepcontrol)

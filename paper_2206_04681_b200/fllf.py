@@ -44,6 +44,11 @@ class fllf_plan_desc(ctypes.Structure):
                 ("k_end", ctypes.c_int), ("include_base", ctypes.c_int), ("device", ctypes.c_int)]
 
 
+class fllf_gain_desc(ctypes.Structure):
+    _fields_ = [("radius", ctypes.c_int), ("m_lo", ctypes.c_double), ("m_hi", ctypes.c_double),
+                ("v_ref", ctypes.c_double)]
+
+
 class fllf_apply_args(ctypes.Structure):
     _fields_ = [("mode", ctypes.c_int), ("a_k", ctypes.POINTER(ctypes.c_double)),
                 ("d_sigma_r", ctypes.c_void_p), ("d_m", ctypes.c_void_p),
@@ -78,6 +83,11 @@ _SIGS = {
                                               ctypes.POINTER(ctypes.c_int),
                                               ctypes.POINTER(ctypes.c_float),
                                               ctypes.POINTER(ctypes.c_int)]),
+    "fllf_rgb_to_yuv": (ctypes.c_int, [_P, _P, ctypes.c_int, ctypes.c_int, ctypes.c_size_t, _P]),
+    "fllf_yuv_to_rgb": (ctypes.c_int, [_P, _P, ctypes.c_int, ctypes.c_int, ctypes.c_size_t, _P]),
+    "fllf_gain_map": (ctypes.c_int, [_P, ctypes.c_size_t, ctypes.c_int, ctypes.c_int,
+                                     ctypes.POINTER(fllf_gain_desc), _P, ctypes.c_size_t, _P]),
+    "fllf_enhance_rgb": (ctypes.c_int, [_P, _P, _P, ctypes.c_size_t, ctypes.POINTER(fllf_gain_desc), _P]),
     "fllf_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "fllf_last_error_message": (ctypes.c_char_p, []),
 }
@@ -222,6 +232,47 @@ def fllf_read_pyramid(plan, frame, level, channel, dst, stream=None) -> None:
 
 def fllf_plan_last_launch_count(plan) -> int:
     return int(lib.fllf_plan_last_launch_count(plan))
+
+
+def _planes3(t, name: str):
+    """(pointer, pitch_bytes, H, W) of a CUDA fp32 (3, H, W) tensor with dense planes."""
+    ptr, pitch = _dev_image(t, name)
+    if t.dim() != 3 or t.shape[0] != 3 or t.stride(0) != t.shape[1] * t.stride(1):
+        raise TypeError(f"{name} must be (3, H, W) with contiguous planes")
+    return ptr, pitch, int(t.shape[1]), int(t.shape[2])
+
+
+def fllf_rgb_to_yuv(rgb, yuv, stream=None) -> None:
+    ip, pitch, H, W = _planes3(rgb, "rgb")
+    op, opitch, _, _ = _planes3(yuv, "yuv")
+    if opitch != pitch:
+        raise ValueError("rgb and yuv must share a pitch")
+    _check(lib.fllf_rgb_to_yuv(ip, op, H, W, pitch, _stream_handle(stream)))
+
+
+def fllf_yuv_to_rgb(yuv, rgb, stream=None) -> None:
+    ip, pitch, H, W = _planes3(yuv, "yuv")
+    op, opitch, _, _ = _planes3(rgb, "rgb")
+    if opitch != pitch:
+        raise ValueError("rgb and yuv must share a pitch")
+    _check(lib.fllf_yuv_to_rgb(ip, op, H, W, pitch, _stream_handle(stream)))
+
+
+def fllf_gain_map(y, m, radius, m_lo, m_hi, v_ref, stream=None) -> None:
+    yp, ypitch = _dev_image(y, "y")
+    mp, mpitch = _dev_image(m, "m")
+    g = fllf_gain_desc(int(radius), float(m_lo), float(m_hi), float(v_ref))
+    _check(lib.fllf_gain_map(yp, ypitch, int(y.shape[-2]), int(y.shape[-1]), ctypes.byref(g), mp, mpitch,
+                             _stream_handle(stream)))
+
+
+def fllf_enhance_rgb(plan, rgb, out, radius, m_lo, m_hi, v_ref, stream=None) -> None:
+    ip, pitch, _, _ = _planes3(rgb, "rgb")
+    op, opitch, _, _ = _planes3(out, "out")
+    if opitch != pitch:
+        raise ValueError("rgb and out must share a pitch")
+    g = fllf_gain_desc(int(radius), float(m_lo), float(m_hi), float(v_ref))
+    _check(lib.fllf_enhance_rgb(plan, ip, op, pitch, ctypes.byref(g), _stream_handle(stream)))
 
 
 KERNEL_KINDS = {0: "build0", 1: "build", 2: "mapbuild", 3: "apply", 4: "apply0"}
