@@ -39,6 +39,9 @@ WORKLOADS = {
                                            "T=510, sigma_r=30, m=3; 64/N frames per rank per step"),
     "config4": dict(cfg=4, frames=1, desc="BASELINE configs[3]: 2160x3840 gray, per-pixel sigma_r/m maps "
                                           "(MAPS mode), 7 levels, K=12; one step = build once + 10 applies"),
+    "color": dict(cfg=3, frames=1, desc="NEXT-3 (Sec. IV, P:373-377): 2160x3840 RGB, YUV, variance gain map "
+                                        "(r=5, m 0.5..3, v_ref 150), Fourier LLF of Y with per-pixel m "
+                                        "(MAPS, 7 levels, K=10, sigma_r=20), back to RGB"),
     "config3": dict(cfg=3, frames=1, desc="BASELINE configs[2]: 2160x3840 RGB (per channel), 7 levels, K=10, "
                                           "T=510, sigma_r=20, m=2; (channel, order) units sharded over N ranks, "
                                           "partial collapse + one NCCL reduce per channel to rank 0"),
@@ -259,6 +262,60 @@ def run_adaptive(args, c, wl, world, rank, local):
     return 0
 
 
+# ------------------------------------------------------------ NEXT-3
+def run_color(args, c, wl, world, rank, local):
+    """Colour enhancement with the variance-driven gain map (fllf_enhance_rgb),
+    one 4K RGB frame per rank per step (replicas, no collective)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2206_04681_b200 import fllf as F
+    from paper_2206_04681_b200 import synth
+
+    H, W, levels, K = c["H"], c["W"], c["levels"], c["K"]
+    rgb = torch.from_numpy(synth.config3_rgb()).cuda()
+    out = torch.empty_like(rgb)
+    l2 = torch.cuda.get_device_properties(local).L2_cache_size or 126 * 2 ** 20
+    flush_buf = torch.empty(2 * l2 // 4 + 1024, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+    plan = F.Plan(H, W, levels, K, c["T"], c["sigma_r"], 1.0)
+    gain = dict(radius=5, m_lo=0.5, m_hi=3.0, v_ref=150.0)
+    for _ in range(max(args.warmup, 1)):
+        flush_buf.zero_()
+        F.fllf_enhance_rgb(plan.handle, rgb, out, stream=stream, **gain)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = ClockSampler(local)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clk.start()
+    for a, b in evs:
+        flush_buf.zero_()
+        a.record(stream)
+        F.fllf_enhance_rgb(plan.handle, rgb, out, stream=stream, **gain)
+        b.record(stream)
+    torch.cuda.synchronize()
+    clk.stop()
+    t = torch.tensor([sum(a.elapsed_time(b) for a, b in evs)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tot_ms = float(t.item())
+    value = world * H * W * args.steps / 1e6 / (tot_ms / 1e3)
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(tot_ms / args.steps, 4), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": wl["desc"], "H": H, "W": W, "levels": levels, "K": K,
+                           "parallelism": f"replica{world}" if world > 1 else "single",
+                           "l2": "flushed between timed steps"},
+                "gpu_launches": args.steps * (3 + (levels - 1) + (levels - 2) + (levels - 1)),
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    clk.close()
+    plan.close()
+    return 0
+
+
 # ------------------------------------------------------------ config 3
 def run_sharded(args, c, wl, world, rank, local):
     """Order-sharded 4K RGB: units (channel, order) split over ranks, partial
@@ -357,6 +414,8 @@ def main():
     wl = WORKLOADS[args.workload]
     c = synth.CONFIGS[wl["cfg"]]
     H, W, levels, K = c["H"], c["W"], c["levels"], c["K"]
+    if args.workload == "color":
+        return run_color(args, c, wl, world, rank, local)
     if wl["cfg"] == 3:
         return run_sharded(args, c, wl, world, rank, local)
     if wl["cfg"] == 4:
