@@ -196,6 +196,24 @@ FLLF_API fllf_status fllf_gain_map(const float* d_y, size_t y_pitch_bytes, int H
 FLLF_API fllf_status fllf_enhance_rgb(fllf_plan p, const float* d_rgb, float* d_rgb_out, size_t pitch_bytes,
                                       const fllf_gain_desc* g, void* s);
 
+/* ---- Naive LLF ground truth (Sec. II-C steps 1-5,
+ * P:143-149, Eq. 13; the reference of the accuracy study, Fig. 4,
+ * P:328-338).  For every level l < l_max and pixel q: g = G_l[I]_q, the image
+ * is remapped around g and the Laplacian coefficient L_l[r(I, g)]_q is taken;
+ * L_lmax = G_lmax[I]; O = collapse (Eq. 4).  remap_mode 0: the exact Gaussian
+ * remap r(i,g) = i + m (i-g) exp(-(i-g)^2 / 2 sigma_r^2) with the plan's
+ * sigma_r, m (reading R1); 1: the truncated series r_K(i,g) = i + sum_k a_k
+ * sin(w_k (i-g)) with the plan's K, T (Fourier LLF with K terms is exactly the
+ * naive LLF of r_K).  Only the pixels each coefficient depends on are
+ * remapped (O(4^l) per coefficient, fp64); a brute-force tool, not a hot
+ * path.  Needs a batch-1 plan with the full order range and include_base,
+ * levels <= FLLF_NAIVE_MAX_LEVELS (TOO_MANY_LEVELS otherwise).  Rebuilds the
+ * plan's pyramids from d_img (like fllf_build_fourier_pyramids) and uses its
+ * level scratch planes.  d_out: H x W fp32, caller-owned. */
+#define FLLF_NAIVE_MAX_LEVELS 5
+FLLF_API fllf_status fllf_naive_llf(fllf_plan p, const float* d_img, size_t pitch_bytes, int remap_mode,
+                                    float* d_out, size_t out_pitch_bytes, void* s);
+
 /* Introspection (tests, tooling). */
 FLLF_API fllf_status fllf_plan_level_dims(fllf_plan p, int level, int* H, int* W);
 FLLF_API fllf_status fllf_workspace_bytes(fllf_plan p, size_t* bytes);

@@ -18,7 +18,7 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libfllf.so")
-SOURCES = ["fllf_host.cpp", "fllf_kernels.cu", "fllf_color.cu"]
+SOURCES = ["fllf_host.cpp", "fllf_kernels.cu", "fllf_color.cu", "fllf_naive.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -793,6 +793,69 @@ fllf_status fllf_enhance_rgb(fllf_plan p, const float* d_rgb, float* d_rgb_out, 
   return FLLF_OK;
 }
 
+// ---------------------------------------------------------------- NEXT-2
+fllf_status fllf_naive_llf(fllf_plan p, const float* d_img, size_t pitch_bytes, int remap_mode, float* d_out,
+                           size_t out_pitch_bytes, void* s) {
+  if (!p) return fail(FLLF_ERR_BAD_POINTER, "NULL plan");
+  if (p->d.batch != 1 || p->kb != 1 || p->KL != p->d.K || !p->d.include_base)
+    return fail(FLLF_ERR_INVALID_ARGUMENT, "naive_llf: needs batch 1, all orders, include_base");
+  if (remap_mode != 0 && remap_mode != 1) return fail(FLLF_ERR_INVALID_ARGUMENT, "naive_llf: remap_mode 0 or 1");
+  if (p->nlev > FLLF_NAIVE_MAX_LEVELS) return fail(FLLF_ERR_TOO_MANY_LEVELS, "naive_llf: levels > FLLF_NAIVE_MAX_LEVELS");
+  long long ipitch, opitch;
+  fllf_status st = check_image(d_img, pitch_bytes, p->d.W, "naive: d_img", &ipitch);
+  if (st != FLLF_OK) return st;
+  st = check_image(d_out, out_pitch_bytes, p->d.W, "naive: d_out", &opitch);
+  if (st != FLLF_OK) return st;
+  st = fllf_build_fourier_pyramids(p, d_img, pitch_bytes, s);
+  if (st != FLLF_OK) return st;
+  DeviceGuard guard(p->device);
+  cudaStream_t stream = static_cast<cudaStream_t>(s);
+  fllf::NaiveParams np{};
+  np.img = d_img;
+  np.img_pitch = ipitch;
+  for (int l = 0; l < p->nlev; ++l) {
+    np.Hs[l] = p->Hs[l];
+    np.Ws[l] = p->Ws[l];
+    if (l >= 1) {
+      np.G[l] = p->lv[l].G;
+      np.gpitch[l] = p->lv[l].pitch;
+      np.L[l] = p->lv[l].D;
+      np.lpitch[l] = p->lv[l].pitch;
+    }
+  }
+  np.L[0] = d_out;
+  np.lpitch[0] = opitch;
+  np.mode = remap_mode;
+  np.K = p->d.K;
+  np.m = p->d.m;
+  np.inv2s2 = 1.0 / (2.0 * p->d.sigma_r * p->d.sigma_r);
+  {
+    std::vector<double> om(p->d.K), ak(p->d.K);
+    fllf_coefficients(p->d.K, p->d.T, p->d.sigma_r, p->d.m, om.data(), ak.data());
+    for (int k = 0; k < p->d.K; ++k) {
+      np.omega[k] = om[k];
+      np.a[k] = ak[k];
+    }
+  }
+  const int lmax = p->nlev - 1;
+  for (int l = 0; l < lmax; ++l) {
+    np.level = l;
+    cudaError_t e = fllf::launch_naive_level(np, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "naive level launch");
+  }
+  // collapse (Eq. 4): O_l = L_l + up(O_{l+1}), O_lmax = G_lmax
+  for (int l = lmax - 1; l >= 0; --l) {
+    float* fine = l == 0 ? d_out : p->lv[l].D;
+    const long long fp = l == 0 ? opitch : p->lv[l].pitch;
+    const float* coarse = (l + 1 == lmax) ? p->lv[l + 1].G : p->lv[l + 1].D;
+    cudaError_t e = fllf::launch_collapse_up(fine, fp, coarse, p->lv[l + 1].pitch, p->Hs[l], p->Ws[l], p->Hs[l + 1],
+                                             p->Ws[l + 1], stream);
+    if (e != cudaSuccess) return cuda_fail(e, "collapse launch");
+  }
+  p->last_launches += 2 * lmax;
+  return FLLF_OK;
+}
+
 fllf_status fllf_plan_level_dims(fllf_plan p, int level, int* H, int* W) {
   if (!p || !H || !W) return fail(FLLF_ERR_BAD_POINTER, "NULL argument");
   if (level < 0 || level >= p->nlev) return fail(FLLF_ERR_INVALID_ARGUMENT, "level out of range");

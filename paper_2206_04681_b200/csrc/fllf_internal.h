@@ -117,6 +117,25 @@ cudaError_t launch_yuv_to_rgb(const ColorParams& p, cudaStream_t s);
 cudaError_t launch_gain_map(const GainParams& p, cudaStream_t s);
 cudaError_t launch_fill(float* ptr, long long pitch, int H, int W, float v, cudaStream_t s);
 
+// Naive LLF ground truth (fllf_naive.cu), one launch per level.
+struct NaiveParams {
+  const float* img;     // level-0 image
+  long long img_pitch;  // floats
+  const float* G[FLLF_MAX_LEVELS];  // G_l[I] planes (l >= 1)
+  long long gpitch[FLLF_MAX_LEVELS];
+  int Hs[FLLF_MAX_LEVELS + 1], Ws[FLLF_MAX_LEVELS + 1];
+  float* L[FLLF_MAX_LEVELS];        // output coefficient planes L_l[O]
+  long long lpitch[FLLF_MAX_LEVELS];
+  int level;            // l of this launch
+  int mode;             // 0: exact Gaussian remap; 1: truncated series r_K
+  int K;
+  double m, inv2s2;     // exact remap: m, 1/(2 sigma_r^2)
+  double a[FLLF_MAX_K], omega[FLLF_MAX_K];  // series remap
+};
+cudaError_t launch_naive_level(const NaiveParams& p, cudaStream_t s);
+cudaError_t launch_collapse_up(float* fine, long long fpitch, const float* coarse, long long cpitch, int Hf, int Wf,
+                               int Hc, int Wc, cudaStream_t s);
+
 // Kernel launchers (fllf_kernels.cu).  Return cudaGetLastError() after launch.
 // pdl: launch with programmatic stream serialization (the kernel may start
 // while its predecessor is still running; it synchronises with griddepcontrol)

@@ -88,6 +88,7 @@ _SIGS = {
     "fllf_gain_map": (ctypes.c_int, [_P, ctypes.c_size_t, ctypes.c_int, ctypes.c_int,
                                      ctypes.POINTER(fllf_gain_desc), _P, ctypes.c_size_t, _P]),
     "fllf_enhance_rgb": (ctypes.c_int, [_P, _P, _P, ctypes.c_size_t, ctypes.POINTER(fllf_gain_desc), _P]),
+    "fllf_naive_llf": (ctypes.c_int, [_P, _P, ctypes.c_size_t, ctypes.c_int, _P, ctypes.c_size_t, _P]),
     "fllf_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "fllf_last_error_message": (ctypes.c_char_p, []),
 }
@@ -273,6 +274,17 @@ def fllf_enhance_rgb(plan, rgb, out, radius, m_lo, m_hi, v_ref, stream=None) -> 
         raise ValueError("rgb and out must share a pitch")
     g = fllf_gain_desc(int(radius), float(m_lo), float(m_hi), float(v_ref))
     _check(lib.fllf_enhance_rgb(plan, ip, op, pitch, ctypes.byref(g), _stream_handle(stream)))
+
+
+FLLF_NAIVE_MAX_LEVELS = 5
+REMAP_EXACT, REMAP_SERIES = 0, 1
+
+
+def fllf_naive_llf(plan, img, out, remap_mode=REMAP_EXACT, stream=None) -> None:
+    """Naive LLF ground truth (NEXT-2) of a CUDA fp32 (H, W) image on a batch-1 plan."""
+    ip, ipitch = _dev_image(img, "img")
+    op, opitch = _dev_image(out, "out")
+    _check(lib.fllf_naive_llf(plan, ip, ipitch, int(remap_mode), op, opitch, _stream_handle(stream)))
 
 
 KERNEL_KINDS = {0: "build0", 1: "build", 2: "mapbuild", 3: "apply", 4: "apply0"}
