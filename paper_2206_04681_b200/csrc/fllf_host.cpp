@@ -98,6 +98,12 @@ struct fllf_plan_s {
   bool tm_ok = false;
   CUtensorMap tmc[FLLF_MAX_LEVELS];
   CUtensorMap tmf[FLLF_MAX_LEVELS];
+  CUtensorMap tmG[FLLF_MAX_LEVELS];  // G_l planes, box 120 x 8 (tile header g rows)
+  CUtensorMap tmD[FLLF_MAX_LEVELS];  // D_l planes, box 68 x 6 (tile header D rows)
+  CUtensorMap tmI;                   // the image of the last build (level-0 g rows)
+  bool tmI_ok = false;
+  const float* tmI_ptr = nullptr;
+  long long tmI_pitch = 0;
 };
 
 namespace {
@@ -127,6 +133,22 @@ bool encode_z_map(CUtensorMap* m, const fllf::DevLevel& L, int planes, unsigned 
   const cuuint32_t estr[3] = {1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// A real fp32 plane stack as a 3-D tensor: W floats x H rows x planes, row
+// stride pitch floats, plane stride fstride floats; box (bx, by, 1).
+bool encode_real_map(CUtensorMap* m, const float* base, int W, int H, int planes, long long pitch,
+                     long long fstride, unsigned bx, unsigned by) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || ((pitch * 4) & 15) || ((fstride * 4) & 15)) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)planes};
+  const cuuint64_t strides[2] = {(cuuint64_t)pitch * 4, (cuuint64_t)fstride * 4};
+  const cuuint32_t box[3] = {bx, by, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -338,8 +360,10 @@ fllf_status fllf_plan_create_ex(const fllf_plan_desc* din, fllf_plan* out) {
   {
     bool ok = true;
     for (int l = 1; l < d.levels && ok; ++l) {
-      ok = encode_z_map(&p->tmc[l], p->lv[l], (int)B * p->KL, 128, 6) &&
-           encode_z_map(&p->tmf[l], p->lv[l], (int)B * p->KL, 256, 8);
+      const fllf::DevLevel& L = p->lv[l];
+      ok = encode_z_map(&p->tmc[l], L, (int)B * p->KL, 128, 6) && encode_z_map(&p->tmf[l], L, (int)B * p->KL, 256, 8) &&
+           encode_real_map(&p->tmG[l], L.G, L.W, L.H, (int)B, L.pitch, L.fstride_r, 120, 8) &&
+           encode_real_map(&p->tmD[l], L.D, L.W, L.H, (int)B, L.pitch, L.fstride_r, 68, 6);
     }
     const char* nt = std::getenv("FLLF_NO_TENSOR_TMA");
     p->tm_ok = ok && !(nt && nt[0] == '1');
@@ -554,9 +578,27 @@ fllf_status fllf_apply(fllf_plan p, const fllf_apply_args* a, float* d_out, size
     if (l > 0) ap.fine = p->lv[l];
     ap.coarse = p->lv[l + 1];
     ap.use_tm = p->tm_ok ? 1 : 0;
+    ap.use_tm_g = ap.use_tm_d = 0;
     if (p->tm_ok) {
       ap.tm_coarse = p->tmc[l + 1];
-      if (l > 0) ap.tm_fine = p->tmf[l];
+      ap.tm_d = p->tmD[l + 1];
+      ap.use_tm_d = 1;
+      if (l > 0) {
+        ap.tm_fine = p->tmf[l];
+        ap.tm_g = p->tmG[l];
+        ap.use_tm_g = 1;
+      } else {
+        if (p->tmI_ptr != p->img || p->tmI_pitch != p->img_pitch) {
+          p->tmI_ok = encode_real_map(&p->tmI, p->img, p->d.W, p->d.H, p->d.batch, p->img_pitch,
+                                      p->img_pitch * p->d.H, 120, 8);
+          p->tmI_ptr = p->img;
+          p->tmI_pitch = p->img_pitch;
+        }
+        if (p->tmI_ok) {
+          ap.tm_g = p->tmI;
+          ap.use_tm_g = 1;
+        }
+      }
     }
     ap.Hf = p->Hs[l];
     ap.Wf = p->Ws[l];

@@ -64,7 +64,10 @@ struct ApplyParams {
   // (k_apply_cl); use_tm = 0 -> per-row bulk copies only.
   CUtensorMap tm_coarse;
   CUtensorMap tm_fine;
+  CUtensorMap tm_g;    // g rows of the tile header: I (level 0) or G_l, box 120 floats x 8 rows
+  CUtensorMap tm_d;    // D_{l+1} rows of the tile header, box 68 floats x 6 rows
   int use_tm;
+  int use_tm_g, use_tm_d;
   DevImage img;        // level-0 input image I (LEVEL0 kernels)
   float* out;          // level-0 output O (LEVEL0 kernels)
   long long out_pitch; // floats

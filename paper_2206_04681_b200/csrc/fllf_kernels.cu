@@ -1151,7 +1151,15 @@ __global__ void __launch_bounds__(160, 3) k_apply_cl(const __grid_constant__ App
       const int hb = nt & 1;
       unsigned char* hdr = smem + HOFF + hb * HDR_BYTES;
       if (nt >= 2) mbar_wait_parity(&hempty[hb], ((nt >> 1) & 1) ^ 1u);
-      if (tma_g) {
+      // interior tiles: the 8 fine g rows / 6 coarse D rows are contiguous -> one tensor copy each
+      const bool tmg = P.use_tm_g && 2 * T.r0 + 7 <= P.Hf - 1;
+      if (tmg) {
+        if (elect_one()) {
+          mbar_arrive_expect_tx(&gfull[hb], 8 * HDR_G_ROW);
+          tma_load_3d(hdr, &P.tm_g, 120 * T.jb, 2 * T.r0, T.frame, &gfull[hb]);
+        }
+        __syncwarp();
+      } else if (tma_g) {
         const float* gb;
         long long gp;
         int wlim;
@@ -1231,10 +1239,14 @@ __global__ void __launch_bounds__(160, 3) k_apply_cl(const __grid_constant__ App
         const float* db = P.coarse.D + T.frame * P.coarse.fstride_r + (60 * T.jb - 4);
         if (elect_one()) {
           mbar_arrive_expect_tx(&dfull[hb], 6 * HDR_D_ROW);
+          if (P.use_tm_d && tmc) {
+            tma_load_3d(hdr + HDR_D_OFF, &P.tm_d, 60 * T.jb - 4, T.r0 - 1, T.frame, &dfull[hb]);
+          } else {
 #pragma unroll
-          for (int q = 0; q < 6; ++q)
-            tma_load_1d(hdr + HDR_D_OFF + q * HDR_D_ROW, db + (long long)crow[q] * P.coarse.pitch, HDR_D_ROW,
-                        &dfull[hb]);
+            for (int q = 0; q < 6; ++q)
+              tma_load_1d(hdr + HDR_D_OFF + q * HDR_D_ROW, db + (long long)crow[q] * P.coarse.pitch, HDR_D_ROW,
+                          &dfull[hb]);
+          }
         }
         __syncwarp();
       }
@@ -1394,7 +1406,11 @@ __global__ void __launch_bounds__(160, 3) k_apply_cl(const __grid_constant__ App
       float dq[3][2];
       mbar_wait_parity(&dfull[hb], hph);
       const int c0 = 60 * T.jb - 4;
-      const int cc0 = upmap(2 * j, P.Wc, P.Wf) - c0, cc1 = upmap(2 * j + 1, P.Wc, P.Wf) - c0;
+      int cc0 = 2 * lane + 2, cc1 = 2 * lane + 3;  // interior column tiles: no border mapping
+      if (T.jb == 0 || T.jb == it.nx - 1) {
+        cc0 = upmap(2 * j, P.Wc, P.Wf) - c0;
+        cc1 = upmap(2 * j + 1, P.Wc, P.Wf) - c0;
+      }
       const float* dh = reinterpret_cast<const float*>(hdr + HDR_D_OFF + warp * HDR_D_ROW);
 #pragma unroll
       for (int tt = 0; tt < 3; ++tt) {
