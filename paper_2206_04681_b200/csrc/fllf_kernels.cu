@@ -110,6 +110,12 @@ __device__ __forceinline__ float2 cmul_sc(float2 a, float2 b) {
 __device__ __forceinline__ float2 cmul_cs(float2 a, float2 b) {
   return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
 }
+// base + off (float2 elements, 32-bit unsigned offset) as one IMAD.WIDE.U32
+__device__ __forceinline__ float2* wide_off(float2* base, unsigned off) {
+  float2* r;
+  asm("mad.wide.u32 %0, %1, 8, %2;" : "=l"(r) : "r"(off), "l"(base));
+  return r;
+}
 __device__ __forceinline__ float2 ldg2(const float* p) { return __ldg(reinterpret_cast<const float2*>(p)); }
 __device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 __device__ __forceinline__ float4 ldg4(const float2* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
@@ -592,7 +598,7 @@ struct Build0Warp {
         const float2 ea = padd(Pc[i][0], zc[0]);
         const float2 eb = padd(Pc[i][1], zc[1]);
         const float2 h = hsum_c(ea, eb);
-        float2* q = zdst + (unsigned)(off0 + i * (int)P.dst.kstride_z);  // IMAD.WIDE.U32
+        float2* q = wide_off(zdst, (unsigned)(off0 + i * (int)P.dst.kstride_z));
         if (store_lane) q[0] = h;
         if (EDGE) {
           if (halo_l) q[-2] = h;  // x == 1: column -1
