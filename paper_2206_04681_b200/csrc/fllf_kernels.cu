@@ -110,6 +110,10 @@ __device__ __forceinline__ float2 cmul_sc(float2 a, float2 b) {
 __device__ __forceinline__ float2 cmul_cs(float2 a, float2 b) {
   return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
 }
+// global store of a float2 (the address came through inline PTX, so say "global")
+__device__ __forceinline__ void stg2(float2* q, float2 v) {
+  asm volatile("st.global.v2.f32 [%0], {%1, %2};" ::"l"(q), "f"(v.x), "f"(v.y) : "memory");
+}
 // base + off (float2 elements, 32-bit unsigned offset) as one IMAD.WIDE.U32
 __device__ __forceinline__ float2* wide_off(float2* base, unsigned off) {
   float2* r;
@@ -599,7 +603,7 @@ struct Build0Warp {
         const float2 eb = padd(Pc[i][1], zc[1]);
         const float2 h = hsum_c(ea, eb);
         float2* q = wide_off(zdst, (unsigned)(off0 + i * (int)P.dst.kstride_z));
-        if (store_lane) q[0] = h;
+        if (store_lane) stg2(q, h);
         if (EDGE) {
           if (halo_l) q[-2] = h;  // x == 1: column -1
           if (halo_r) q[P.Wc - x] = h;
