@@ -33,3 +33,15 @@ run(259, 130, 7, 1)
 run(64, 33, 2, 10, k_begin=3, k_end=8, include_base=False)
 run(40, 52, 4, 7, batch=3)
 print("sanitize target done")
+
+# NEXT-3 colour pipeline and NEXT-2 naive LLF
+rgb = torch.rand((3, 61, 90), device="cuda") * 255
+out = torch.empty_like(rgb)
+with F.Plan(61, 90, 4, 8, 510.0, 30.0, 1.0) as p:
+    F.fllf_enhance_rgb(p.handle, rgb, out, 3, 0.5, 3.0, 120.0)
+    img = rgb[0].contiguous()
+    o2 = torch.empty_like(img)
+    F.fllf_naive_llf(p.handle, img, o2, F.REMAP_EXACT)
+    torch.cuda.synchronize()
+assert torch.isfinite(out).all() and torch.isfinite(o2).all()
+print("sanitize target (colour, naive) done")
