@@ -93,6 +93,16 @@ typedef struct {
                        partials of a partition of 1..K and adding I gives O (Eq. 4 is
                        linear).                                                           */
   int device;       /* CUDA device ordinal; -1 (default) = the current device            */
+  int row_begin;    /* row band [row_begin, row_end) of the frame this plan computes      */
+  int row_end;      /*   (NEXT-1, multi-GPU row split); 0,0 = the whole frame (default).
+                       Both multiples of 2^(levels-1) (row_end may be H); batch must be
+                       1.  Rows are global: d_img / d_out point at row row_begin, and
+                       d_img must also hold the 2 rows above and below the band
+                       (where they exist).  The pyramids are stored for the band plus
+                       2 halo rows per side per level; the halo rows of the levels >= 1
+                       are the neighbour bands' rows, exchanged by the caller between the
+                       per-level calls (fllf_build_level / fllf_apply_level /
+                       fllf_plan_band_plane).  SCALAR / COEFFS only.                    */
 } fllf_plan_desc;
 
 /* Per-apply arguments; NULL means FLLF_SCALAR. */
@@ -213,6 +223,28 @@ FLLF_API fllf_status fllf_enhance_rgb(fllf_plan p, const float* d_rgb, float* d_
 #define FLLF_NAIVE_MAX_LEVELS 5
 FLLF_API fllf_status fllf_naive_llf(fllf_plan p, const float* d_img, size_t pitch_bytes, int remap_mode,
                                     float* d_out, size_t out_pitch_bytes, void* s);
+
+/* ---- Per-level execution for row bands (NEXT-1; north star: "Large frames
+ * can instead be split into row bands with halo exchange").  The level
+ * recursions of Eq. 1 (build, fine to coarse) and Eq. 14 + Eq. 4 (apply,
+ * coarse to fine) only couple neighbouring rows through the 5-tap stencil
+ * (2 rows) and the up-sampling (1 row), so a band needs, per level, 2 halo
+ * rows of G_l and Z_l (after the build of level l) and of D_l (after the apply
+ * of level l) from its neighbours.
+ *   fllf_build_level(p, d_img, pitch, l, s): build step l -> l+1 (l = 0..levels-2).
+ *   fllf_apply_level(p, a, d_out, pitch, l, s): apply level l (call l = levels-2
+ *     down to 0; SCALAR / COEFFS).
+ *   fllf_plan_band_plane(p, l, kind, ...): the device layout of the stored
+ *     rows of level l (kind 0 = G_l, 1 = Z_l complex planes incl. halo columns,
+ *     2 = D_l): pointer to the first stored row `first_row` (global index),
+ *     `rows` stored rows, row pitch, `planes` planes (orders x frames for Z) and
+ *     the plane stride.  Rows [first_row, first_row + rows) minus the band's own
+ *     rows are the halo rows the caller fills. */
+FLLF_API fllf_status fllf_build_level(fllf_plan p, const float* d_img, size_t pitch_bytes, int level, void* s);
+FLLF_API fllf_status fllf_apply_level(fllf_plan p, const fllf_apply_args* a, float* d_out, size_t out_pitch_bytes,
+                                      int level, void* s);
+FLLF_API fllf_status fllf_plan_band_plane(fllf_plan p, int level, int kind, void** d_ptr, size_t* pitch_bytes,
+                                          int* first_row, int* rows, int* planes, size_t* plane_stride_bytes);
 
 /* Introspection (tests, tooling). */
 FLLF_API fllf_status fllf_plan_level_dims(fllf_plan p, int level, int* H, int* W);

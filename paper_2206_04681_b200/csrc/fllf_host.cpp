@@ -61,6 +61,10 @@ struct fllf_plan_s {
   int device = 0;
   int nlev = 0;
   int Hs[FLLF_MAX_LEVELS]{}, Ws[FLLF_MAX_LEVELS]{};
+  // row band (NEXT-1): own rows [bb[l], be[l]) and allocated rows [al[l], ah[l]]
+  // (own rows + up to 2 halo rows per side) of every level, global indices
+  bool band = false;
+  int bb[FLLF_MAX_LEVELS]{}, be[FLLF_MAX_LEVELS]{}, al[FLLF_MAX_LEVELS]{}, ah[FLLF_MAX_LEVELS]{};
   fllf::DevLevel lv[FLLF_MAX_LEVELS]{};
   void* ws = nullptr;
   size_t ws_bytes = 0;
@@ -254,7 +258,7 @@ fllf_status fllf_plan_create(int H, int W, int levels, int K, double T, double s
                              fllf_plan* out) {
   fllf_plan_desc d{};
   d.H = H; d.W = W; d.levels = levels; d.K = K; d.T = T; d.sigma_r = sigma_r; d.m = m;
-  d.batch = 1; d.k_begin = 0; d.k_end = 0; d.include_base = 1; d.device = -1;
+  d.batch = 1; d.k_begin = 0; d.k_end = 0; d.include_base = 1; d.device = -1; d.row_begin = 0; d.row_end = 0;
   return fllf_plan_create_ex(&d, out);
 }
 
@@ -277,6 +281,16 @@ fllf_status fllf_plan_create_ex(const fllf_plan_desc* din, fllf_plan* out) {
   if (d.k_begin < 1 || d.k_end <= d.k_begin || d.k_end > d.K + 1)
     return fail(FLLF_ERR_INVALID_ARGUMENT, "order range must satisfy 1 <= k_begin < k_end <= K+1");
   if (d.levels > FLLF_MAX_LEVELS) return fail(FLLF_ERR_TOO_MANY_LEVELS, "levels > FLLF_MAX_LEVELS");
+  if (d.row_begin == 0 && d.row_end == 0) d.row_end = d.H;
+  {
+    const int align = 1 << (d.levels - 1);
+    if (d.row_begin < 0 || d.row_end <= d.row_begin || d.row_end > d.H)
+      return fail(FLLF_ERR_INVALID_ARGUMENT, "row band must satisfy 0 <= row_begin < row_end <= H");
+    if (d.row_begin % align || (d.row_end != d.H && d.row_end % align))
+      return fail(FLLF_ERR_INVALID_ARGUMENT, "row band boundaries must be multiples of 2^(levels-1) (or H)");
+    if ((d.row_begin != 0 || d.row_end != d.H) && d.batch != 1)
+      return fail(FLLF_ERR_INVALID_ARGUMENT, "row bands need batch 1");
+  }
   int h = d.H, w = d.W;
   for (int l = 1; l < d.levels; ++l) {
     h = (h + 1) / 2;
@@ -320,6 +334,13 @@ fllf_status fllf_plan_create_ex(const fllf_plan_desc* din, fllf_plan* out) {
     p->Hs[l] = (p->Hs[l - 1] + 1) / 2;
     p->Ws[l] = (p->Ws[l - 1] + 1) / 2;
   }
+  p->band = d.row_begin != 0 || d.row_end != d.H;
+  for (int l = 0; l < d.levels; ++l) {
+    p->bb[l] = d.row_begin >> l;
+    p->be[l] = d.row_end == d.H ? p->Hs[l] : d.row_end >> l;
+    p->al[l] = std::max(0, p->bb[l] - 2);
+    p->ah[l] = std::min(p->Hs[l], p->be[l] + 2) - 1;
+  }
   // workspace layout: per level l >= 1: G | D | Z  (each 256-byte aligned)
   const size_t B = (size_t)d.batch;
   size_t off = 0;
@@ -332,8 +353,9 @@ fllf_status fllf_plan_create_ex(const fllf_plan_desc* din, fllf_plan* out) {
     L.W = p->Ws[l];
     L.pitch = (int)pitch;
     L.zpitch = (int)zpitch;
-    L.fstride_r = (long long)(L.H * pitch);
-    L.kstride_z = (long long)(L.H * zpitch);
+    const int rows = p->ah[l] - p->al[l] + 1;  // allocated rows (all of them without a band)
+    L.fstride_r = (long long)rows * pitch;
+    L.kstride_z = (long long)rows * zpitch;
     L.fstride_z = (long long)p->KL * L.kstride_z;
     offG[l] = off;
     off = align_up(off + B * L.fstride_r * sizeof(float), 256);
@@ -353,9 +375,11 @@ fllf_status fllf_plan_create_ex(const fllf_plan_desc* din, fllf_plan* out) {
   }
   char* base = static_cast<char*>(p->ws);
   for (int l = 1; l < d.levels; ++l) {
-    p->lv[l].G = reinterpret_cast<float*>(base + offG[l]);
-    p->lv[l].D = reinterpret_cast<float*>(base + offD[l]);
-    p->lv[l].Z = reinterpret_cast<float2*>(base + offZ[l]) + fllf::ZHALO;
+    // plane pointers address GLOBAL row indices: row al[l] is the first allocated row
+    fllf::DevLevel& L = p->lv[l];
+    L.G = reinterpret_cast<float*>(base + offG[l]) - (long long)p->al[l] * L.pitch;
+    L.D = reinterpret_cast<float*>(base + offD[l]) - (long long)p->al[l] * L.pitch;
+    L.Z = reinterpret_cast<float2*>(base + offZ[l]) + fllf::ZHALO - (long long)p->al[l] * L.zpitch;
   }
   {
     bool ok = true;
@@ -411,6 +435,38 @@ static fllf_status check_image(const void* ptr, size_t pitch_bytes, int W, const
   return FLLF_OK;
 }
 
+// One build step, level l -> l+1 (l = 0 from the image).  `img` is the
+// row-0 (virtual for bands) image pointer, pitch in floats.
+static fllf_status build_level_impl(fllf_plan p, const float* img, long long pitch, int l, cudaStream_t stream,
+                                    bool pdl) {
+  fllf::BuildParams bp{};
+  bp.img.p = img;
+  bp.img.H = p->d.H;
+  bp.img.W = p->d.W;
+  bp.img.pitch = pitch;
+  bp.img.fstride = pitch * p->d.H;
+  if (l > 0) bp.src = p->lv[l];
+  bp.dst = p->lv[l + 1];
+  bp.Hf = p->Hs[l];
+  bp.Wf = p->Ws[l];
+  bp.Hc = p->Hs[l + 1];
+  bp.Wc = p->Ws[l + 1];
+  bp.KL = p->KL;
+  bp.kbase = p->kb;
+  bp.maps = 0;
+  bp.invT = (float)(1.0 / p->d.T);
+  bp.o_begin = p->bb[l + 1];
+  bp.o_end = p->be[l + 1];
+  bp.fr_lo = p->al[l];
+  bp.fr_hi = p->ah[l];
+  cudaError_t e;
+  {
+    ProfScope ps(p, stream, l == 0 ? FLLF_K_BUILD0 : FLLF_K_BUILD, l);
+    e = fllf::launch_build(bp, l, p->d.batch, stream, pdl);
+  }
+  return e == cudaSuccess ? FLLF_OK : cuda_fail(e, "build kernel launch");
+}
+
 fllf_status fllf_build_fourier_pyramids(fllf_plan p, const float* d_img, size_t pitch_bytes, void* s) {
   if (!p) return fail(FLLF_ERR_BAD_POINTER, "NULL plan");
   long long pitch;
@@ -418,39 +474,38 @@ fllf_status fllf_build_fourier_pyramids(fllf_plan p, const float* d_img, size_t 
   if (st != FLLF_OK) return st;
   DeviceGuard guard(p->device);
   cudaStream_t stream = static_cast<cudaStream_t>(s);
-  const double T = p->d.T;
+  const float* img = d_img - (long long)p->d.row_begin * pitch;  // global row 0 (bands: virtual)
   int launches = 0;
   p->nrec = 0;
   p->last_was_apply = false;
   for (int l = 0; l + 1 < p->nlev; ++l) {
-    fllf::BuildParams bp{};
-    bp.img.p = d_img;
-    bp.img.H = p->d.H;
-    bp.img.W = p->d.W;
-    bp.img.pitch = pitch;
-    bp.img.fstride = pitch * p->d.H;
-    if (l > 0) bp.src = p->lv[l];
-    bp.dst = p->lv[l + 1];
-    bp.Hf = p->Hs[l];
-    bp.Wf = p->Ws[l];
-    bp.Hc = p->Hs[l + 1];
-    bp.Wc = p->Ws[l + 1];
-    bp.KL = p->KL;
-    bp.kbase = p->kb;
-    bp.maps = 0;
-    bp.invT = (float)(1.0 / T);
-    cudaError_t e;
-    {
-      ProfScope ps(p, stream, l == 0 ? FLLF_K_BUILD0 : FLLF_K_BUILD, l);
-      e = fllf::launch_build(bp, l, p->d.batch, stream, p->use_pdl && l > 0);
-    }
-    if (e != cudaSuccess) return cuda_fail(e, "build kernel launch");
+    st = build_level_impl(p, img, pitch, l, stream, p->use_pdl && l > 0 && !p->band);
+    if (st != FLLF_OK) return st;
     ++launches;
   }
   p->built = true;
-  p->img = d_img;
+  p->img = img;
   p->img_pitch = pitch;
   p->last_launches = launches;
+  return FLLF_OK;
+}
+
+fllf_status fllf_build_level(fllf_plan p, const float* d_img, size_t pitch_bytes, int level, void* s) {
+  if (!p) return fail(FLLF_ERR_BAD_POINTER, "NULL plan");
+  if (level < 0 || level + 1 >= p->nlev) return fail(FLLF_ERR_INVALID_ARGUMENT, "build_level: level out of range");
+  long long pitch;
+  fllf_status st = check_image(d_img, pitch_bytes, p->d.W, "build_level: d_img", &pitch);
+  if (st != FLLF_OK) return st;
+  DeviceGuard guard(p->device);
+  const float* img = d_img - (long long)p->d.row_begin * pitch;
+  if (level == 0) p->nrec = 0;
+  p->last_was_apply = false;
+  st = build_level_impl(p, img, pitch, level, static_cast<cudaStream_t>(s), false);
+  if (st != FLLF_OK) return st;
+  p->img = img;
+  p->img_pitch = pitch;
+  p->last_launches = 1;
+  if (level + 2 == p->nlev) p->built = true;
   return FLLF_OK;
 }
 
@@ -475,7 +530,59 @@ static fllf_status ensure_maps_ws(fllf_plan p) {
   return FLLF_OK;
 }
 
-fllf_status fllf_apply(fllf_plan p, const fllf_apply_args* a, float* d_out, size_t out_pitch_bytes, void* s) {
+// One apply level (coarse to fine; l = lmax-1 .. 0) with the prepared parameters.
+static fllf_status apply_level_impl(fllf_plan p, fllf::ApplyParams& ap, int l, bool maps, cudaStream_t stream,
+                                    bool pdl) {
+  const int lmax = p->nlev - 1;
+  if (l > 0) ap.fine = p->lv[l];
+  ap.coarse = p->lv[l + 1];
+  ap.use_tm = p->tm_ok ? 1 : 0;
+  ap.use_tm_g = ap.use_tm_d = 0;
+  if (p->tm_ok) {
+    ap.tm_coarse = p->tmc[l + 1];
+    ap.tm_d = p->tmD[l + 1];
+    ap.use_tm_d = 1;
+    if (l > 0) {
+      ap.tm_fine = p->tmf[l];
+      ap.tm_g = p->tmG[l];
+      ap.use_tm_g = 1;
+    } else {
+      if (p->tmI_ptr != p->img || p->tmI_pitch != p->img_pitch) {
+        p->tmI_ok = encode_real_map(&p->tmI, p->img, p->d.W, p->d.H, p->d.batch, p->img_pitch,
+                                    p->img_pitch * p->d.H, 120, 8);
+        p->tmI_ptr = p->img;
+        p->tmI_pitch = p->img_pitch;
+      }
+      if (p->tmI_ok) {
+        ap.tm_g = p->tmI;
+        ap.use_tm_g = 1;
+      }
+    }
+  }
+  ap.Hf = p->Hs[l];
+  ap.Wf = p->Ws[l];
+  ap.Hc = p->Hs[l + 1];
+  ap.Wc = p->Ws[l + 1];
+  ap.r_begin = p->bb[l + 1];
+  ap.r_end = p->be[l + 1];
+  ap.cr_lo = p->al[l + 1];
+  ap.cr_hi = p->ah[l + 1];
+  ap.fr_lo = p->al[l];
+  ap.fr_hi = p->ah[l];
+  const bool has_d = (l + 1) < lmax;  // D_lmax = 0
+  ap.wait_first = (l == lmax - 1 || !pdl) ? 1 : 0;
+  cudaError_t e;
+  {
+    ProfScope ps(p, stream, l == 0 ? FLLF_K_APPLY0 : FLLF_K_APPLY, l);
+    e = fllf::launch_apply(ap, l, has_d, maps, p->d.batch, stream, pdl);
+  }
+  return e == cudaSuccess ? FLLF_OK : cuda_fail(e, "apply kernel launch");
+}
+
+// fllf_apply (only_level < 0: the whole coarse-to-fine pass) and
+// fllf_apply_level (only that level).
+static fllf_status apply_impl(fllf_plan p, const fllf_apply_args* a, float* d_out, size_t out_pitch_bytes, void* s,
+                              int only_level) {
   if (!p) return fail(FLLF_ERR_BAD_POINTER, "NULL plan");
   if (!p->built) return fail(FLLF_ERR_NOT_BUILT, "fllf_apply before fllf_build_fourier_pyramids");
   long long opitch;
@@ -484,6 +591,9 @@ fllf_status fllf_apply(fllf_plan p, const fllf_apply_args* a, float* d_out, size
   const int mode = a ? a->mode : FLLF_SCALAR;
   if (mode != FLLF_SCALAR && mode != FLLF_COEFFS && mode != FLLF_MAPS)
     return fail(FLLF_ERR_INVALID_ARGUMENT, "apply: unknown mode");
+  if (mode == FLLF_MAPS && p->band) return fail(FLLF_ERR_INVALID_ARGUMENT, "apply(MAPS) is not supported on row bands");
+  if (only_level >= 0 && mode == FLLF_MAPS) return fail(FLLF_ERR_INVALID_ARGUMENT, "apply_level: MAPS not supported");
+  if (only_level >= p->nlev - 1) return fail(FLLF_ERR_INVALID_ARGUMENT, "apply_level: level out of range");
   DeviceGuard guard(p->device);
   cudaStream_t stream = static_cast<cudaStream_t>(s);
   const double T = p->d.T;
@@ -495,7 +605,7 @@ fllf_status fllf_apply(fllf_plan p, const fllf_apply_args* a, float* d_out, size
   ap.img.W = p->d.W;
   ap.img.pitch = p->img_pitch;
   ap.img.fstride = p->img_pitch * p->d.H;
-  ap.out = d_out;
+  ap.out = d_out - (long long)p->d.row_begin * opitch;  // global row 0 (bands: virtual)
   ap.out_pitch = opitch;
   ap.out_fstride = opitch * p->d.H;
   ap.KL = p->KL;
@@ -563,6 +673,10 @@ fllf_status fllf_apply(fllf_plan p, const fllf_apply_args* a, float* d_out, size
       bp.KL = 0;
       bp.kbase = p->kb;
       bp.maps = 1;
+      bp.o_begin = 0;
+      bp.o_end = p->Hs[l + 1];
+      bp.fr_lo = 0;
+      bp.fr_hi = p->Hs[l] - 1;
       bp.invT = (float)(1.0 / T);
       cudaError_t e;
       {
@@ -575,46 +689,47 @@ fllf_status fllf_apply(fllf_plan p, const fllf_apply_args* a, float* d_out, size
   }
   const int lmax = p->nlev - 1;
   for (int l = lmax - 1; l >= 0; --l) {
-    if (l > 0) ap.fine = p->lv[l];
-    ap.coarse = p->lv[l + 1];
-    ap.use_tm = p->tm_ok ? 1 : 0;
-    ap.use_tm_g = ap.use_tm_d = 0;
-    if (p->tm_ok) {
-      ap.tm_coarse = p->tmc[l + 1];
-      ap.tm_d = p->tmD[l + 1];
-      ap.use_tm_d = 1;
-      if (l > 0) {
-        ap.tm_fine = p->tmf[l];
-        ap.tm_g = p->tmG[l];
-        ap.use_tm_g = 1;
-      } else {
-        if (p->tmI_ptr != p->img || p->tmI_pitch != p->img_pitch) {
-          p->tmI_ok = encode_real_map(&p->tmI, p->img, p->d.W, p->d.H, p->d.batch, p->img_pitch,
-                                      p->img_pitch * p->d.H, 120, 8);
-          p->tmI_ptr = p->img;
-          p->tmI_pitch = p->img_pitch;
-        }
-        if (p->tmI_ok) {
-          ap.tm_g = p->tmI;
-          ap.use_tm_g = 1;
-        }
-      }
-    }
-    ap.Hf = p->Hs[l];
-    ap.Wf = p->Ws[l];
-    ap.Hc = p->Hs[l + 1];
-    ap.Wc = p->Ws[l + 1];
-    const bool has_d = (l + 1) < lmax;  // D_lmax = 0
-    ap.wait_first = (l == lmax - 1) ? 1 : 0;
-    cudaError_t e;
-    {
-      ProfScope ps(p, stream, l == 0 ? FLLF_K_APPLY0 : FLLF_K_APPLY, l);
-      e = fllf::launch_apply(ap, l, has_d, maps, p->d.batch, stream, p->use_pdl);
-    }
-    if (e != cudaSuccess) return cuda_fail(e, "apply kernel launch");
+    if (only_level >= 0 && l != only_level) continue;
+    st = apply_level_impl(p, ap, l, maps, stream, p->use_pdl && !p->band && only_level < 0);
+    if (st != FLLF_OK) return st;
     ++launches;
   }
   p->last_launches = launches;
+  return FLLF_OK;
+}
+
+fllf_status fllf_apply(fllf_plan p, const fllf_apply_args* a, float* d_out, size_t out_pitch_bytes, void* s) {
+  return apply_impl(p, a, d_out, out_pitch_bytes, s, -1);
+}
+
+fllf_status fllf_apply_level(fllf_plan p, const fllf_apply_args* a, float* d_out, size_t out_pitch_bytes, int level,
+                             void* s) {
+  if (level < 0) return fail(FLLF_ERR_INVALID_ARGUMENT, "apply_level: level out of range");
+  return apply_impl(p, a, d_out, out_pitch_bytes, s, level);
+}
+
+fllf_status fllf_plan_band_plane(fllf_plan p, int level, int kind, void** d_ptr, size_t* pitch_bytes, int* first_row,
+                                 int* rows, int* planes, size_t* plane_stride_bytes) {
+  if (!p || !d_ptr || !pitch_bytes || !first_row || !rows || !planes || !plane_stride_bytes)
+    return fail(FLLF_ERR_BAD_POINTER, "band_plane: NULL argument");
+  if (level < 1 || level >= p->nlev || kind < 0 || kind > 2)
+    return fail(FLLF_ERR_INVALID_ARGUMENT, "band_plane: level 1..levels-1, kind 0 (G), 1 (Z), 2 (D)");
+  const fllf::DevLevel& L = p->lv[level];
+  const int lo = p->al[level];
+  *first_row = lo;
+  *rows = p->ah[level] - lo + 1;
+  if (kind == 1) {
+    *d_ptr = const_cast<float2*>(L.Z - fllf::ZHALO + (long long)lo * L.zpitch);
+    *pitch_bytes = (size_t)L.zpitch * sizeof(float2);
+    *planes = p->KL * p->d.batch;
+    *plane_stride_bytes = (size_t)L.kstride_z * sizeof(float2);
+  } else {
+    const float* b = kind == 0 ? L.G : L.D;
+    *d_ptr = const_cast<float*>(b + (long long)lo * L.pitch);
+    *pitch_bytes = (size_t)L.pitch * sizeof(float);
+    *planes = p->d.batch;
+    *plane_stride_bytes = (size_t)L.fstride_r * sizeof(float);
+  }
   return FLLF_OK;
 }
 
@@ -780,7 +895,7 @@ fllf_status fllf_gain_map(const float* d_y, size_t y_pitch_bytes, int H, int W, 
 fllf_status fllf_enhance_rgb(fllf_plan p, const float* d_rgb, float* d_rgb_out, size_t pitch_bytes,
                              const fllf_gain_desc* g, void* s) {
   if (!p) return fail(FLLF_ERR_BAD_POINTER, "NULL plan");
-  if (p->d.batch != 1) return fail(FLLF_ERR_INVALID_ARGUMENT, "enhance_rgb: plan batch must be 1");
+  if (p->d.batch != 1 || p->band) return fail(FLLF_ERR_INVALID_ARGUMENT, "enhance_rgb: plan batch must be 1, full frame");
   fllf_status st = check_gain(g);
   if (st != FLLF_OK) return st;
   const int H = p->d.H, W = p->d.W;
@@ -839,8 +954,8 @@ fllf_status fllf_enhance_rgb(fllf_plan p, const float* d_rgb, float* d_rgb_out, 
 fllf_status fllf_naive_llf(fllf_plan p, const float* d_img, size_t pitch_bytes, int remap_mode, float* d_out,
                            size_t out_pitch_bytes, void* s) {
   if (!p) return fail(FLLF_ERR_BAD_POINTER, "NULL plan");
-  if (p->d.batch != 1 || p->kb != 1 || p->KL != p->d.K || !p->d.include_base)
-    return fail(FLLF_ERR_INVALID_ARGUMENT, "naive_llf: needs batch 1, all orders, include_base");
+  if (p->d.batch != 1 || p->kb != 1 || p->KL != p->d.K || !p->d.include_base || p->band)
+    return fail(FLLF_ERR_INVALID_ARGUMENT, "naive_llf: needs batch 1, all orders, include_base, full frame");
   if (remap_mode != 0 && remap_mode != 1) return fail(FLLF_ERR_INVALID_ARGUMENT, "naive_llf: remap_mode 0 or 1");
   if (p->nlev > FLLF_NAIVE_MAX_LEVELS) return fail(FLLF_ERR_TOO_MANY_LEVELS, "naive_llf: levels > FLLF_NAIVE_MAX_LEVELS");
   long long ipitch, opitch;
@@ -916,6 +1031,7 @@ fllf_status fllf_read_pyramid(fllf_plan p, int frame, int level, int channel, fl
                               size_t dst_pitch_bytes, void* s) {
   if (!p || !d_dst) return fail(FLLF_ERR_BAD_POINTER, "NULL argument");
   if (!p->built) return fail(FLLF_ERR_NOT_BUILT, "read_pyramid before build");
+  if (p->band) return fail(FLLF_ERR_INVALID_ARGUMENT, "read_pyramid: use fllf_plan_band_plane on row bands");
   if (level < 1 || level >= p->nlev || frame < 0 || frame >= p->d.batch || channel < 0 || channel > p->KL)
     return fail(FLLF_ERR_INVALID_ARGUMENT, "read_pyramid: frame/level/channel out of range");
   DeviceGuard guard(p->device);

@@ -55,6 +55,14 @@ struct BuildParams {
   int rows_per_strip;  // coarse rows per warp
   int maps;            // 1: build the (sigma, m) map pyramids instead of G/Z
   float invT;          // 1/T
+  // Row bands (NEXT-1; full frame: o_begin = 0, o_end = Hc, fr_lo = 0,
+  // fr_hi = Hf-1).  Rows are GLOBAL level indices everywhere (the plane
+  // pointers are offset so that a global row addresses the band's rows);
+  // outputs are the coarse rows [o_begin, o_end); fine-row reads are clamped
+  // to the allocated rows [fr_lo, fr_hi] (band + halo), which only ever
+  // changes rows that feed no stored output.
+  int o_begin, o_end;
+  int fr_lo, fr_hi;
 };
 
 struct ApplyParams {
@@ -94,6 +102,12 @@ struct ApplyParams {
   // [0] = (-a/64, a/64) even row, even col; [1] = (-a/16, a/16) mixed;
   // [2] = (-a/4, a/4) odd row, odd col; [3] = (a, -a) same-level Z (l >= 1).
   float2 cw[FLLF_MAX_K][4];
+  // Row bands (see BuildParams): tiles cover the coarse rows [r_begin, r_end);
+  // coarse-plane (Z_{l+1}, D_{l+1}) reads are clamped to [cr_lo, cr_hi],
+  // fine-plane reads (Z_l, G_l or I) to [fr_lo, fr_hi]; tensor-map copies are
+  // used only for boxes inside those ranges.
+  int r_begin, r_end;
+  int cr_lo, cr_hi, fr_lo, fr_hi;
 };
 
 // Colour conversion (fllf_color.cu): three planes in, three planes out, all

@@ -235,7 +235,7 @@ struct BuildWarp {
   }
 
   __device__ __forceinline__ void load_row(int row, Row& d) const {
-    const int rr = refl101(row, P.Hf);
+    const int rr = min(max(refl101(row, P.Hf), P.fr_lo), P.fr_hi);
 #pragma unroll
     for (int i = 0; i < NR; ++i) {
       const float* rp = rsrc[i] + (long long)rr * rpitch;
@@ -416,9 +416,9 @@ __global__ void __launch_bounds__(32) k_build(const BuildParams P) {
   pdl_trigger();  // let the next kernel get scheduled
   const int cb = blockIdx.x;  // one warp per CTA: all control flow is blockIdx-uniform
   if (cb * 30 >= P.Wc) return;
-  const int o0 = blockIdx.y * P.rows_per_strip;
-  if (o0 >= P.Hc) return;
-  const int R = min(P.rows_per_strip, P.Hc - o0);
+  const int o0 = P.o_begin + blockIdx.y * P.rows_per_strip;
+  if (o0 >= P.o_end) return;
+  const int R = min(P.rows_per_strip, P.o_end - o0);
   // level 0: chunk-major (CTAs are dispatched in blockIdx order, so resident
   // warps mostly run the same code variant -- instruction-cache locality);
   // above: frame-major (L2 locality of the shared G plane)
@@ -530,7 +530,7 @@ struct Build0Warp {
       const int r0 = 2 * (o0 + p - 1);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const float* rp = isrc + (long long)refl101(r0 + h, P.Hf) * ipitch;
+        const float* rp = isrc + (long long)min(max(refl101(r0 + h, P.Hf), P.fr_lo), P.fr_hi) * ipitch;
         float2* d = h ? d1 : d0;
         if (EDGE) {
           cp_async4(&d->x, rp + rc0);
@@ -630,7 +630,7 @@ struct Build0Warp {
   // pair R+1), PD pairs in flight through the shared-memory ring.
   __device__ __forceinline__ void run(int R) {
     // pairs 0 .. R+1+PD are read: rows 2(o0-1) .. 2(o0+R+PD)+1
-    rows_in = o0 >= 1 && 2 * (o0 + R + PD) + 1 < P.Hf;
+    rows_in = o0 >= 1 && 2 * (o0 - 1) >= P.fr_lo && 2 * (o0 + R + PD) + 1 <= P.fr_hi;
     rowp = isrc + (long long)(2 * (o0 - 1)) * ipitch;
 #pragma unroll
     for (int q = 0; q < PD; ++q) issue_pair(q);
@@ -658,9 +658,9 @@ __global__ void __launch_bounds__(32, 16) k_build0(const BuildParams P) {
   pdl_trigger();
   const int cb = blockIdx.x;
   if (cb * 30 >= P.Wc) return;
-  const int o0 = blockIdx.y * P.rows_per_strip;
-  if (o0 >= P.Hc) return;
-  const int R = min(P.rows_per_strip, P.Hc - o0);
+  const int o0 = P.o_begin + blockIdx.y * P.rows_per_strip;
+  if (o0 >= P.o_end) return;
+  const int R = min(P.rows_per_strip, P.o_end - o0);
   const int nframes = gridDim.z / P.nchunks;
   const int chunk = blockIdx.z / nframes;
   const int frame = blockIdx.z % nframes;
@@ -702,11 +702,11 @@ struct ApplyTile {
   int jb, r0, frame;
 };
 __device__ __forceinline__ ApplyTile apply_tile(int t, const ApplyParams& P) {
-  const int nx = (P.Wf + 119) / 120, ny = (P.Hc + 3) / 4;
+  const int nx = (P.Wf + 119) / 120, ny = (P.r_end - P.r_begin + 3) / 4;
   ApplyTile T;
   T.jb = t % nx;
   t /= nx;
-  T.r0 = (t % ny) * 4;
+  T.r0 = P.r_begin + (t % ny) * 4;
   T.frame = t / ny;
   return T;
 }
@@ -718,17 +718,19 @@ struct TileIter {
   ApplyTile T;
   __device__ __forceinline__ TileIter(const ApplyParams& P) {
     nx = (P.Wf + 119) / 120;
-    ny = (P.Hc + 3) / 4;
+    ny = (P.r_end - P.r_begin + 3) / 4;
+    rb0 = P.r_begin;
     const int q = gridDim.x / nx;
     dj = gridDim.x - q * nx;
     dr = q % ny;
     df = q / ny;
     T = apply_tile(blockIdx.x, P);
-    T.r0 >>= 2;  // row block index while iterating
+    T.r0 = (T.r0 - rb0) >> 2;  // row block index while iterating
   }
+  int rb0;
   __device__ __forceinline__ ApplyTile tile() const {
     ApplyTile u = T;
-    u.r0 *= 4;
+    u.r0 = rb0 + u.r0 * 4;
     return u;
   }
   __device__ __forceinline__ void next() {
@@ -1162,7 +1164,7 @@ __global__ void __launch_bounds__(160, 3) k_apply_cl(const __grid_constant__ App
       unsigned char* hdr = smem + HOFF + hb * HDR_BYTES;
       if (nt >= 2) mbar_wait_parity(&hempty[hb], ((nt >> 1) & 1) ^ 1u);
       // interior tiles: the 8 fine g rows / 6 coarse D rows are contiguous -> one tensor copy each
-      const bool tmg = P.use_tm_g && 2 * T.r0 + 7 <= P.Hf - 1;
+      const bool tmg = P.use_tm_g && 2 * T.r0 + 7 <= min(P.Hf - 1, P.fr_hi);
       if (tmg) {
         if (elect_one()) {
           mbar_arrive_expect_tx(&gfull[hb], 8 * HDR_G_ROW);
@@ -1187,7 +1189,7 @@ __global__ void __launch_bounds__(160, 3) k_apply_cl(const __grid_constant__ App
           mbar_arrive_expect_tx(&gfull[hb], 8 * gbytes);
 #pragma unroll
           for (int q = 0; q < 8; ++q)
-            tma_load_1d(hdr + q * HDR_G_ROW, gb + (long long)min(2 * T.r0 + q, P.Hf - 1) * gp + 120 * T.jb, gbytes,
+            tma_load_1d(hdr + q * HDR_G_ROW, gb + (long long)min(2 * T.r0 + q, P.fr_hi) * gp + 120 * T.jb, gbytes,
                         &gfull[hb]);
         }
         __syncwarp();
@@ -1195,11 +1197,11 @@ __global__ void __launch_bounds__(160, 3) k_apply_cl(const __grid_constant__ App
       const float2* zc0 = P.coarse.Z + T.frame * P.coarse.fstride_z + (60 * T.jb - 2);
       int crow[6];
 #pragma unroll
-      for (int q = 0; q < 6; ++q) crow[q] = upmap(T.r0 - 1 + q, P.Hc, P.Hf);
+      for (int q = 0; q < 6; ++q) crow[q] = min(max(upmap(T.r0 - 1 + q, P.Hc, P.Hf), P.cr_lo), P.cr_hi);
       const float2* zf0 = LEVEL0 ? nullptr : P.fine.Z + T.frame * P.fine.fstride_z + (120 * T.jb - 4);
       // interior tiles: the 6 coarse (8 fine) rows are contiguous -> one tensor copy per order
-      const bool tmc = P.use_tm && T.r0 >= 1 && T.r0 + 4 <= P.Hc - 1;
-      const bool tmf = !LEVEL0 && P.use_tm && 2 * T.r0 + 7 <= P.Hf - 1;
+      const bool tmc = P.use_tm && T.r0 >= 1 && T.r0 - 1 >= P.cr_lo && T.r0 + 4 <= min(P.Hc - 1, P.cr_hi);
+      const bool tmf = !LEVEL0 && P.use_tm && 2 * T.r0 + 7 <= min(P.Hf - 1, P.fr_hi);
       const int xc = 2 * (ZHALO + 60 * T.jb - 2), xf = 2 * (ZHALO + 120 * T.jb - 4);  // float columns
 #pragma unroll 1
       for (int i = KL - 1; i >= 0; i -= OPS) {
@@ -1228,7 +1230,7 @@ __global__ void __launch_bounds__(160, 3) k_apply_cl(const __grid_constant__ App
 #pragma unroll
                   for (int q = 0; q < 8; ++q)
                     tma_load_1d(so + FOFF + q * FROW_BYTES,
-                                zf + (long long)min(2 * T.r0 + q, P.Hf - 1) * P.fine.zpitch, FROW_BYTES, &full[s]);
+                                zf + (long long)min(2 * T.r0 + q, P.fr_hi) * P.fine.zpitch, FROW_BYTES, &full[s]);
                 }
               }
             }
@@ -1281,7 +1283,7 @@ __global__ void __launch_bounds__(160, 3) k_apply_cl(const __grid_constant__ App
     const unsigned char* hdr = smem + HOFF + hb * HDR_BYTES;
     const int r = T.r0 + warp;
     const int j = T.jb * 30 + lane - 1;  // coarse columns 2j, 2j+1 -> fine columns 4j..4j+3
-    const bool act = r < P.Hc && lane >= 1 && lane <= 30 && 4 * j < P.Wf;
+    const bool act = r < P.r_end && lane >= 1 && lane <= 30 && 4 * j < P.Wf;
     float g[8];
     if (tma_g) {
       mbar_wait_parity(&gfull[hb], hph);
@@ -1296,7 +1298,7 @@ __global__ void __launch_bounds__(160, 3) k_apply_cl(const __grid_constant__ App
       const float* base = P.img.p + T.frame * P.img.fstride;
 #pragma unroll
       for (int tt = 0; tt < 2; ++tt) {
-        const float* rp = base + (long long)min(2 * rr + tt, P.Hf - 1) * P.img.pitch;
+        const float* rp = base + (long long)min(2 * rr + tt, P.fr_hi) * P.img.pitch;
 #pragma unroll
         for (int q = 0; q < 4; ++q) g[4 * tt + q] = __ldg(rp + min(max(xf0 + q, 0), P.Wf - 1));
       }
@@ -1512,8 +1514,9 @@ template <int NC, bool FROM_IMAGE>
 static cudaError_t launch_build_nc(BuildParams p, int batch, cudaStream_t s, bool pdl) {
   const int bx = (p.Wc + 29) / 30;  // one warp (CTA) per 30 coarse columns
   p.nchunks = p.KL / NC;
-  p.rows_per_strip = pick_rows(p.Hc, bx, batch * p.nchunks);
-  dim3 grid(bx, (p.Hc + p.rows_per_strip - 1) / p.rows_per_strip, batch * p.nchunks);
+  const int nrows = p.o_end - p.o_begin;
+  p.rows_per_strip = pick_rows(nrows, bx, batch * p.nchunks);
+  dim3 grid(bx, (nrows + p.rows_per_strip - 1) / p.rows_per_strip, batch * p.nchunks);
   if (p.rows_per_strip == 2) return launch_ex(k_build<NC, 1, FROM_IMAGE, true>, grid, dim3(32), 0, s, pdl, p);
   return launch_ex(k_build<NC, 1, FROM_IMAGE, false>, grid, dim3(32), 0, s, pdl, p);
 }
@@ -1525,10 +1528,10 @@ static cudaError_t launch_build0_nc(BuildParams p, int batch, cudaStream_t s, bo
   // strips of >= 4 output rows (the run loop needs R >= 2; halo rows 3/(2R))
   int R = 16;
   { const char* e = std::getenv("FLLF_B0_WARPS"); const long long tw = e ? std::atoll(e) : 148LL * 8;
-    while (R > 4 && (long long)bx * ((p.Hc + R - 1) / R) * batch * p.nchunks < tw) R >>= 1; }
-  if (R > p.Hc) R = std::max(p.Hc, 2);
+    while (R > 4 && (long long)bx * ((p.o_end - p.o_begin + R - 1) / R) * batch * p.nchunks < tw) R >>= 1; }
+  if (R > p.o_end - p.o_begin) R = std::max(p.o_end - p.o_begin, 2);
   p.rows_per_strip = R;
-  dim3 grid(bx, (p.Hc + R - 1) / R, batch * p.nchunks);
+  dim3 grid(bx, (p.o_end - p.o_begin + R - 1) / R, batch * p.nchunks);
   return launch_ex(k_build0<NC>, grid, dim3(32), 0, s, pdl, p);
 }
 
@@ -1544,8 +1547,8 @@ cudaError_t launch_build(const BuildParams& p0, int level_src, int batch, cudaSt
   if (p.maps) {
     const int bx = (p.Wc + 29) / 30;
     p.nchunks = 1;
-    p.rows_per_strip = pick_rows(p.Hc, bx, 1);
-    dim3 grid(bx, (p.Hc + p.rows_per_strip - 1) / p.rows_per_strip, 1);
+    p.rows_per_strip = pick_rows(p.o_end - p.o_begin, bx, 1);
+    dim3 grid(bx, (p.o_end - p.o_begin + p.rows_per_strip - 1) / p.rows_per_strip, 1);
     if (level_src == 0) return launch_ex(k_build<0, 2, true, false>, grid, dim3(32), 0, s, pdl, p);
     return launch_ex(k_build<0, 2, false, false>, grid, dim3(32), 0, s, pdl, p);
   }
@@ -1611,7 +1614,7 @@ static int sm_count() {
 
 template <bool L0, bool HD, bool MP>
 static cudaError_t launch_apply_t(const ApplyParams& p, int batch, cudaStream_t s, bool pdl) {
-  const int ntiles = ((p.Wf + 119) / 120) * ((p.Hc + 3) / 4) * batch;
+  const int ntiles = ((p.Wf + 119) / 120) * ((p.r_end - p.r_begin + 3) / 4) * batch;
   const int per_sm = MP ? 2 : 3;  // resident CTAs per SM (launch bounds)
   dim3 grid(std::min(ntiles, sm_count() * per_sm));
   const int smem = apply_stages<L0>() * apply_stage_bytes<L0>();
@@ -1626,7 +1629,7 @@ static cudaError_t launch_apply_t(const ApplyParams& p, int batch, cudaStream_t 
 
 template <bool L0, bool HD>
 static cudaError_t launch_apply_cl_t(const ApplyParams& p, int batch, cudaStream_t s, bool pdl) {
-  const int ntiles = ((p.Wf + 119) / 120) * ((p.Hc + 3) / 4) * batch;
+  const int ntiles = ((p.Wf + 119) / 120) * ((p.r_end - p.r_begin + 3) / 4) * batch;
   dim3 grid(std::min(ntiles, sm_count() * 3));
   const int smem = apply_cl_smem<L0>();
   static bool attr_set = false;

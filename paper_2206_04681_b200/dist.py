@@ -116,3 +116,164 @@ def gpu_partial_fn(img, levels: int, K: int, T: float, sigma_r: float, m: float)
 
     fn.plans = plans
     return fn
+
+
+# ------------------------------------------------------------------ NEXT-1
+# Row-band split with per-level halo exchange (north star: "Large frames can
+# instead be split into row bands with halo exchange").  Every level of both
+# passes only couples neighbouring rows: the build of level l+1 reads fine rows
+# 2o-2 .. 2o+2 (Eq. 1, 5-tap), the apply of level l reads the coarse rows
+# r-1 .. r+1 of Z_{l+1} and D_{l+1} (up-sampling).  A band therefore needs two
+# halo rows per side of G_l, Z_l (after the build of level l) and of D_l
+# (after the apply of level l), exchanged between neighbouring bands only --
+# no collective over the whole frame, and the traffic per level is
+# 4 rows x (2K+2) planes x W_l x 4 B, independent of the number of bands.
+
+BAND_G, BAND_Z, BAND_D = 0, 1, 2
+
+
+def band_partition(H: int, levels: int, world: int) -> List[tuple]:
+    """Contiguous row bands [row_begin, row_end) with boundaries at multiples of
+    2^(levels-1) (so every level's band is a whole number of rows) and at least
+    2 own rows per band at the coarsest level; balanced to one alignment unit."""
+    align = 1 << (levels - 1)
+    units = -(-H // align)
+    if units < 2 * world:
+        raise ValueError(f"{H} rows at {levels} levels allow at most {units // 2} bands")
+    out = []
+    for r in range(world):
+        f, c = frame_partition(units, world, r)
+        out.append((f * align, min((f + c) * align, H)))
+    return out
+
+
+def band_level_rows(H: int, levels: int, band: tuple, level: int) -> tuple:
+    """The band's own rows [b, e) at `level` (global indices, ceil-halving)."""
+    h = H
+    for _ in range(level):
+        h = (h + 1) // 2
+    rb, re_ = band
+    return rb >> level, (h if re_ == H else re_ >> level)
+
+
+def band_schedule(levels: int) -> list:
+    """Per-level steps of one band: ('build', l) makes level l+1; ('xchg', l,
+    kinds) refreshes the halo rows of level l; ('apply', l) is the apply of l."""
+    steps = []
+    for l in range(levels - 1):
+        steps.append(("build", l))
+        steps.append(("xchg", l + 1, (BAND_G, BAND_Z)))
+    for l in range(levels - 2, -1, -1):
+        if l + 1 < levels - 1:
+            steps.append(("xchg", l + 1, (BAND_D,)))
+        steps.append(("apply", l))
+    return steps
+
+
+def halo_slices(first_row: int, rows: int, own: tuple):
+    """Row indices (into a stored-rows view starting at global `first_row`) of
+    the top halo, the bottom halo, the first two own rows and the last two."""
+    b, e = own
+    top = slice(0, b - first_row)
+    bot = slice(e - first_row, rows)
+    n_top, n_bot = top.stop - top.start, bot.stop - bot.start
+    send_up = slice(b - first_row, b - first_row + 2)
+    send_dn = slice(e - first_row - 2, e - first_row)
+    return top, bot, send_up, send_dn, n_top, n_bot
+
+
+def exchange_halos(view, first_row: int, own: tuple, group=None, up: int = None, down: int = None):
+    """Fill the halo rows of `view` (planes, rows, floats: a band's stored rows of
+    one plane kind and level) from the neighbouring ranks `up` / `down` (None at
+    the frame border), sending them this band's edge rows; NCCL / gloo p2p."""
+    import torch.distributed as dist
+
+    top, bot, send_up, send_dn, n_top, n_bot = halo_slices(first_row, view.shape[1], own)
+    ops, recv = [], []
+    if up is not None:
+        ops.append(dist.P2POp(dist.isend, view[:, send_up].contiguous(), up, group))
+        buf = view.new_empty((view.shape[0], n_top, view.shape[2]))
+        ops.append(dist.P2POp(dist.irecv, buf, up, group))
+        recv.append((top, buf))
+    if down is not None:
+        ops.append(dist.P2POp(dist.isend, view[:, send_dn].contiguous(), down, group))
+        buf = view.new_empty((view.shape[0], n_bot, view.shape[2]))
+        ops.append(dist.P2POp(dist.irecv, buf, down, group))
+        recv.append((bot, buf))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+    for sl, buf in recv:
+        view[:, sl] = buf
+
+
+class GpuBand:
+    """One rank's band: a libfllf plan over rows [row_begin, row_end) of an
+    H x W frame and the per-level execution of `band_schedule`."""
+
+    def __init__(self, H, W, levels, K, T, sigma_r, m, band, device=0):
+        from . import fllf as F
+        self.F, self.H, self.levels, self.band, self.device = F, H, levels, band, device
+        self.plan = F.Plan(H, W, levels, K, T, sigma_r, m, row_begin=band[0], row_end=band[1])
+
+    def view(self, level, kind):
+        return self.F.band_rows_view(self.plan.handle, level, kind, self.device)
+
+    def own(self, level):
+        return band_level_rows(self.H, self.levels, self.band, level)
+
+    def run_step(self, step, img_ptr, img_pitch, out_ptr, out_pitch, stream=None):
+        if step[0] == "build":
+            self.F.fllf_build_level(self.plan.handle, img_ptr, img_pitch, step[1], stream)
+        elif step[0] == "apply":
+            self.F.fllf_apply_level(self.plan.handle, out_ptr, out_pitch, step[1], stream=stream)
+
+    def close(self):
+        self.plan.close()
+
+
+def band_filter(gb: GpuBand, img_band, out_band, group=None):
+    """Row-band Fourier LLF on this rank.  img_band: CUDA (rows, W) tensor holding
+    the band's rows plus the 2 rows above / below it (where they exist);
+    out_band: (row_end - row_begin, W).  Neighbours are ranks rank-1 / rank+1."""
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    up = rank - 1 if rank > 0 else None
+    down = rank + 1 if rank + 1 < world else None
+    top_in = gb.band[0] - max(0, gb.band[0] - 2)
+    ipitch = img_band.stride(0) * 4
+    iptr = img_band.data_ptr() + top_in * ipitch
+    for step in band_schedule(gb.levels):
+        if step[0] == "xchg":
+            for kind in step[2]:
+                v, first = gb.view(step[1], kind)
+                exchange_halos(v, first, gb.own(step[1]), group, up, down)
+        else:
+            gb.run_step(step, iptr, ipitch, out_band.data_ptr(), out_band.stride(0) * 4)
+
+
+def band_filter_local(bands: list, img, out):
+    """All bands of one frame on the current GPU (single-process emulation of
+    band_filter, for tests and for one GPU): the same per-level schedule, the
+    halo exchange done as device copies between the bands' stored rows.
+    img / out: CUDA (H, W) tensors of the whole frame."""
+    H = img.shape[0]
+    levels = bands[0].levels
+    ipitch, opitch = img.stride(0) * 4, out.stride(0) * 4
+    for step in band_schedule(levels):
+        if step[0] == "xchg":
+            l = step[1]
+            for kind in step[2]:
+                views = [gb.view(l, kind) for gb in bands]
+                for i in range(len(bands) - 1):
+                    (vu, fu), (vd, fd) = views[i], views[i + 1]
+                    ou, od = bands[i].own(l), bands[i + 1].own(l)
+                    _, bot_u, _, send_dn_u, _, _ = halo_slices(fu, vu.shape[1], ou)
+                    top_d, _, send_up_d, _, _, _ = halo_slices(fd, vd.shape[1], od)
+                    vu[:, bot_u] = vd[:, send_up_d]
+                    vd[:, top_d] = vu[:, send_dn_u]
+        else:
+            for gb in bands:
+                rb = gb.band[0]
+                gb.run_step(step, img.data_ptr() + rb * ipitch, ipitch, out.data_ptr() + rb * opitch, opitch)

@@ -41,7 +41,8 @@ class fllf_plan_desc(ctypes.Structure):
     _fields_ = [("H", ctypes.c_int), ("W", ctypes.c_int), ("levels", ctypes.c_int),
                 ("K", ctypes.c_int), ("T", ctypes.c_double), ("sigma_r", ctypes.c_double),
                 ("m", ctypes.c_double), ("batch", ctypes.c_int), ("k_begin", ctypes.c_int),
-                ("k_end", ctypes.c_int), ("include_base", ctypes.c_int), ("device", ctypes.c_int)]
+                ("k_end", ctypes.c_int), ("include_base", ctypes.c_int), ("device", ctypes.c_int),
+                ("row_begin", ctypes.c_int), ("row_end", ctypes.c_int)]
 
 
 class fllf_gain_desc(ctypes.Structure):
@@ -89,6 +90,13 @@ _SIGS = {
                                      ctypes.POINTER(fllf_gain_desc), _P, ctypes.c_size_t, _P]),
     "fllf_enhance_rgb": (ctypes.c_int, [_P, _P, _P, ctypes.c_size_t, ctypes.POINTER(fllf_gain_desc), _P]),
     "fllf_naive_llf": (ctypes.c_int, [_P, _P, ctypes.c_size_t, ctypes.c_int, _P, ctypes.c_size_t, _P]),
+    "fllf_build_level": (ctypes.c_int, [_P, _P, ctypes.c_size_t, ctypes.c_int, _P]),
+    "fllf_apply_level": (ctypes.c_int, [_P, ctypes.POINTER(fllf_apply_args), _P, ctypes.c_size_t, ctypes.c_int,
+                                        _P]),
+    "fllf_plan_band_plane": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P),
+                                            ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(ctypes.c_int),
+                                            ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                                            ctypes.POINTER(ctypes.c_size_t)]),
     "fllf_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "fllf_last_error_message": (ctypes.c_char_p, []),
 }
@@ -152,9 +160,9 @@ def fllf_plan_create(H, W, levels, K, T, sigma_r, m) -> int:
 
 
 def fllf_plan_create_ex(H, W, levels, K, T, sigma_r=30.0, m=1.0, batch=1, k_begin=0, k_end=0,
-                        include_base=True, device=-1) -> int:
+                        include_base=True, device=-1, row_begin=0, row_end=0) -> int:
     d = fllf_plan_desc(H, W, levels, K, float(T), float(sigma_r), float(m), batch, k_begin, k_end,
-                       1 if include_base else 0, device)
+                       1 if include_base else 0, device, row_begin, row_end)
     h = _P()
     _check(lib.fllf_plan_create_ex(ctypes.byref(d), ctypes.byref(h)))
     return h.value
@@ -185,6 +193,102 @@ def fllf_apply(plan, out, mode=FLLF_SCALAR, a_k=None, sigma_map=None, m_map=None
         args.d_sigma_r, args.d_m, args.map_pitch_bytes = sp, mp, spitch
     _check(lib.fllf_apply(plan, ctypes.byref(args), optr, opitch, _stream_handle(stream)))
     del keep
+
+
+def _apply_args(mode, a_k):
+    args = fllf_apply_args()
+    args.mode = mode
+    keep = None
+    if mode == FLLF_COEFFS:
+        keep = np.ascontiguousarray(np.asarray(a_k, dtype=np.float64))
+        args.a_k = keep.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    elif mode != FLLF_SCALAR:
+        raise ValueError("per-level apply supports SCALAR and COEFFS")
+    return args, keep
+
+
+def fllf_build_level(plan, img_ptr, pitch_bytes, level, stream=None) -> None:
+    """Build step level -> level+1.  img_ptr: device address of the band's first
+    row (global row row_begin) of the image (int), pitch in bytes."""
+    _check(lib.fllf_build_level(plan, int(img_ptr), int(pitch_bytes), int(level), _stream_handle(stream)))
+
+
+def fllf_apply_level(plan, out_ptr, pitch_bytes, level, mode=FLLF_SCALAR, a_k=None, stream=None) -> None:
+    args, keep = _apply_args(mode, a_k)
+    _check(lib.fllf_apply_level(plan, ctypes.byref(args), int(out_ptr), int(pitch_bytes), int(level),
+                                _stream_handle(stream)))
+    del keep
+
+
+BAND_G, BAND_Z, BAND_D = 0, 1, 2
+
+
+def fllf_plan_band_plane(plan, level, kind):
+    """dict(ptr, pitch_bytes, first_row, rows, planes, plane_stride_bytes) of the stored rows."""
+    ptr, pitch, first, rows, planes, pstride = (_P(), ctypes.c_size_t(), ctypes.c_int(), ctypes.c_int(),
+                                                ctypes.c_int(), ctypes.c_size_t())
+    _check(lib.fllf_plan_band_plane(plan, int(level), int(kind), ctypes.byref(ptr), ctypes.byref(pitch),
+                                    ctypes.byref(first), ctypes.byref(rows), ctypes.byref(planes),
+                                    ctypes.byref(pstride)))
+    return dict(ptr=ptr.value, pitch_bytes=pitch.value, first_row=first.value, rows=rows.value,
+                planes=planes.value, plane_stride_bytes=pstride.value)
+
+
+# ---- zero-copy torch views of library-owned device memory (DLPack)
+class _DLDevice(ctypes.Structure):
+    _fields_ = [("device_type", ctypes.c_int), ("device_id", ctypes.c_int)]
+
+
+class _DLDataType(ctypes.Structure):
+    _fields_ = [("code", ctypes.c_uint8), ("bits", ctypes.c_uint8), ("lanes", ctypes.c_uint16)]
+
+
+class _DLTensor(ctypes.Structure):
+    _fields_ = [("data", ctypes.c_void_p), ("device", _DLDevice), ("ndim", ctypes.c_int),
+                ("dtype", _DLDataType), ("shape", ctypes.POINTER(ctypes.c_int64)),
+                ("strides", ctypes.POINTER(ctypes.c_int64)), ("byte_offset", ctypes.c_uint64)]
+
+
+class _DLManagedTensor(ctypes.Structure):
+    pass
+
+
+_DLManagedTensor._fields_ = [("dl_tensor", _DLTensor), ("manager_ctx", ctypes.c_void_p),
+                             ("deleter", ctypes.CFUNCTYPE(None, ctypes.POINTER(_DLManagedTensor)))]
+_keepalive = {}
+
+
+@ctypes.CFUNCTYPE(None, ctypes.POINTER(_DLManagedTensor))
+def _dl_deleter(p):
+    _keepalive.pop(ctypes.addressof(p.contents), None)
+
+
+def device_view(ptr: int, shape, strides, device: int):
+    """float32 torch tensor aliasing `ptr` on CUDA `device` (element strides).
+    The memory stays owned by the library plan; keep the plan alive."""
+    import torch
+    n = len(shape)
+    sh = (ctypes.c_int64 * n)(*shape)
+    st = (ctypes.c_int64 * n)(*strides)
+    mt = _DLManagedTensor()
+    mt.dl_tensor = _DLTensor(ctypes.c_void_p(ptr), _DLDevice(2, device), n, _DLDataType(2, 32, 1), sh, st, 0)
+    mt.manager_ctx = None
+    mt.deleter = _dl_deleter
+    _keepalive[ctypes.addressof(mt)] = (mt, sh, st)
+    pyapi = ctypes.pythonapi
+    pyapi.PyCapsule_New.restype = ctypes.py_object
+    pyapi.PyCapsule_New.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_void_p]
+    cap = pyapi.PyCapsule_New(ctypes.addressof(mt), b"dltensor", None)
+    return torch.utils.dlpack.from_dlpack(cap)
+
+
+def band_rows_view(plan, level, kind, device: int):
+    """torch view (planes, rows, row floats) of the stored rows of one level and its first global row."""
+    d = fllf_plan_band_plane(plan, level, kind)
+    row_floats = d["pitch_bytes"] // 4
+    v = device_view(d["ptr"], (d["planes"], d["rows"], row_floats),
+                    (d["plane_stride_bytes"] // 4, row_floats, 1), device)
+    return v, d["first_row"]
 
 
 def fllf_filter(plan, img, out, stream=None) -> None:
@@ -324,11 +428,13 @@ class Plan:
     k_end: int = 0
     include_base: bool = True
     device: int = -1
+    row_begin: int = 0
+    row_end: int = 0
 
     def __post_init__(self):
         self.handle = fllf_plan_create_ex(self.H, self.W, self.levels, self.K, self.T, self.sigma_r,
                                           self.m, self.batch, self.k_begin, self.k_end,
-                                          self.include_base, self.device)
+                                          self.include_base, self.device, self.row_begin, self.row_end)
 
     def build(self, img, stream=None):
         fllf_build_fourier_pyramids(self.handle, img, stream)

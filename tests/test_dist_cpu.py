@@ -85,3 +85,65 @@ def test_sharded_filter_gloo_equals_full(tmp_path, world):
     from oracle import fllf_oracle as O
     full = np.stack([O.fourier_llf(img[c], *args) for c in range(3)])
     assert np.abs(np.load(res) - full).max() <= 1e-9
+
+
+# ---------------------------------------------------------------- NEXT-1
+def test_band_partition_properties():
+    from paper_2206_04681_b200.dist import band_level_rows, band_partition
+    for H, levels, world in [(2160, 7, 8), (1080, 6, 4), (517, 3, 7), (300, 5, 3), (128, 2, 2)]:
+        bands = band_partition(H, levels, world)
+        align = 1 << (levels - 1)
+        assert bands[0][0] == 0 and bands[-1][1] == H
+        for (a, b), (c, d) in zip(bands, bands[1:]):
+            assert b == c and b % align == 0
+        h = H
+        for l in range(levels):
+            rows = [band_level_rows(H, levels, bd, l) for bd in bands]
+            assert rows[0][0] == 0 and rows[-1][1] == h
+            assert all(e - b >= 2 for b, e in rows)
+            assert all(r1[1] == r2[0] for r1, r2 in zip(rows, rows[1:]))
+            h = (h + 1) // 2
+    with pytest.raises(ValueError):
+        band_partition(100, 6, 4)
+
+
+def _band_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2206_04681_b200.dist import band_level_rows, band_partition, exchange_halos
+    H, levels, W = 300, 4, 5
+    band = band_partition(H, levels, world)[rank]
+    ok = True
+    for l in range(1, levels):
+        b, e = band_level_rows(H, levels, band, l)
+        hl = H
+        for _ in range(l):
+            hl = (hl + 1) // 2
+        lo, hi = max(0, b - 2), min(hl, e + 2)
+        # stored rows: own rows hold their global row index, halos -1
+        v = torch.full((2, hi - lo, W), -1.0)
+        for r in range(b, e):
+            v[:, r - lo] = float(r)
+        exchange_halos(v, lo, (b, e), None, rank - 1 if rank > 0 else None, rank + 1 if rank + 1 < world else None)
+        expect = torch.arange(lo, hi, dtype=torch.float32)[None, :, None].expand_as(v)
+        ok = ok and bool(torch.equal(v, expect))
+    q.put((rank, ok))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_band_halo_exchange_gloo(world):
+    """Every halo row a band stores equals the neighbour's row of the same global index."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ps = [ctx.Process(target=_band_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    assert all(res.values()), res
