@@ -42,6 +42,9 @@ WORKLOADS = {
     "color": dict(cfg=3, frames=1, desc="NEXT-3 (Sec. IV, P:373-377): 2160x3840 RGB, YUV, variance gain map "
                                         "(r=5, m 0.5..3, v_ref 150), Fourier LLF of Y with per-pixel m "
                                         "(MAPS, 7 levels, K=10, sigma_r=20), back to RGB"),
+    "bands": dict(cfg=3, frames=1, desc="NEXT-1: one 2160x3840 gray frame (config-3 channel parameters: 7 levels, "
+                                        "K=10, sigma_r=20, m=2) split into N row bands with per-level halo "
+                                        "exchange (NCCL p2p between neighbouring ranks)"),
     "config3": dict(cfg=3, frames=1, desc="BASELINE configs[2]: 2160x3840 RGB (per channel), 7 levels, K=10, "
                                           "T=510, sigma_r=20, m=2; (channel, order) units sharded over N ranks, "
                                           "partial collapse + one NCCL reduce per channel to rank 0"),
@@ -316,6 +319,75 @@ def run_color(args, c, wl, world, rank, local):
     return 0
 
 
+# ------------------------------------------------------------ NEXT-1
+def run_bands(args, c, wl, world, rank, local):
+    """One 4K frame per step split into `world` row bands (strong scaling): each
+    rank builds / applies its band level by level, exchanging 2 halo rows per
+    level with its neighbours (dist.band_filter); at N = 1 the whole frame."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2206_04681_b200 import dist as D
+    from paper_2206_04681_b200 import synth
+
+    H, W, levels, K = c["H"], c["W"], c["levels"], c["K"]
+    img = torch.from_numpy(synth.config2_image(seed=3000, H=H, W=W)).cuda()
+    if world == 1:
+        band = (0, H)
+    else:
+        band = D.band_partition(H, levels, world)[rank]
+    lo, hi = max(0, band[0] - 2), min(H, band[1] + 2)
+    img_band = img[lo:hi].contiguous()
+    out_band = torch.empty((band[1] - band[0], W), dtype=torch.float32, device="cuda")
+    gb = D.GpuBand(H, W, levels, K, c["T"], c["sigma_r"], c["m"], band, device=local)
+    l2 = torch.cuda.get_device_properties(local).L2_cache_size or 126 * 2 ** 20
+    flush_buf = torch.empty(2 * l2 // 4 + 1024, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        if world == 1:
+            gb.plan.filter(img_band, out_band, stream)
+        else:
+            D.band_filter(gb, img_band, out_band)
+
+    for _ in range(max(args.warmup, 1)):
+        flush_buf.zero_()
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = ClockSampler(local)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clk.start()
+    for a, b in evs:
+        flush_buf.zero_()
+        if world > 1:
+            dist.barrier()
+        a.record(stream)
+        step()
+        b.record(stream)
+    torch.cuda.synchronize()
+    clk.stop()
+    t = torch.tensor([sum(a.elapsed_time(b) for a, b in evs)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tot_ms = float(t.item())
+    value = H * W * args.steps / 1e6 / (tot_ms / 1e3)
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(tot_ms / args.steps, 4), "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": wl["desc"], "H": H, "W": W, "levels": levels, "K": K,
+                           "parallelism": f"row-bands{world}", "l2": "flushed between timed steps"},
+                "gpu_launches": args.steps * 2 * (levels - 1), "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    clk.close()
+    gb.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 # ------------------------------------------------------------ config 3
 def run_sharded(args, c, wl, world, rank, local):
     """Order-sharded 4K RGB: units (channel, order) split over ranks, partial
@@ -416,6 +488,8 @@ def main():
     H, W, levels, K = c["H"], c["W"], c["levels"], c["K"]
     if args.workload == "color":
         return run_color(args, c, wl, world, rank, local)
+    if args.workload == "bands":
+        return run_bands(args, c, wl, world, rank, local)
     if wl["cfg"] == 3:
         return run_sharded(args, c, wl, world, rank, local)
     if wl["cfg"] == 4:
