@@ -1503,8 +1503,16 @@ cudaError_t launch_ex(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_
 // Rows per warp strip: long strips amortise the 3 halo rows; shorter strips
 // only when the grid would leave SMs without warps.
 int pick_rows(int Hc, int blocks_x, int z) {
-  int R = 16;
-  while (R > 2 && (long long)blocks_x * ((Hc + R - 1) / R) * z < 148LL * 8) R >>= 1;
+  static const long long target = [] {
+    const char* e = std::getenv("FLLF_BL_WARPS");
+    return e ? std::atoll(e) : 148LL * 8;
+  }();
+  static const int rmax = [] {
+    const char* e = std::getenv("FLLF_BL_RMAX");
+    return e ? std::atoi(e) : 16;
+  }();
+  int R = rmax;
+  while (R > 2 && (long long)blocks_x * ((Hc + R - 1) / R) * z < target) R >>= 1;
   return R;
 }
 
