@@ -1099,9 +1099,19 @@ template <bool LEVEL0>
 __host__ __device__ constexpr int apply_cl_ops() {
   return LEVEL0 ? 2 : 1;
 }
+// resident CTAs per SM (launch bounds).  A fourth level-0 CTA (96 registers,
+// a few spilled, 6 stages) measured slower on B200 (config 2 apply0 20.8 ->
+// 22.0 us), so 3.
+#ifndef FLLF_APPLY0_CTAS
+#define FLLF_APPLY0_CTAS 3
+#endif
+template <bool LEVEL0>
+__host__ __device__ constexpr int apply_cl_ctas() {
+  return LEVEL0 ? FLLF_APPLY0_CTAS : 3;
+}
 template <bool LEVEL0>
 __host__ __device__ constexpr int apply_cl_stages() {
-  return LEVEL0 ? 8 : 5;
+  return LEVEL0 ? (FLLF_APPLY0_CTAS >= 4 ? 6 : 8) : 5;
 }
 template <bool LEVEL0>
 __host__ __device__ constexpr int apply_cl_smem() {
@@ -1109,7 +1119,7 @@ __host__ __device__ constexpr int apply_cl_smem() {
 }
 
 template <bool LEVEL0, bool HAS_D>
-__global__ void __launch_bounds__(160, 3) k_apply_cl(const __grid_constant__ ApplyParams P, const int ntiles) {
+__global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0>()) k_apply_cl(const __grid_constant__ ApplyParams P, const int ntiles) {
   constexpr int S = apply_cl_stages<LEVEL0>();
   constexpr int OPS = apply_cl_ops<LEVEL0>();
   constexpr int OBYTES = apply_stage_bytes<LEVEL0>();  // one order
@@ -1638,7 +1648,7 @@ static cudaError_t launch_apply_t(const ApplyParams& p, int batch, cudaStream_t 
 template <bool L0, bool HD>
 static cudaError_t launch_apply_cl_t(const ApplyParams& p, int batch, cudaStream_t s, bool pdl) {
   const int ntiles = ((p.Wf + 119) / 120) * ((p.r_end - p.r_begin + 3) / 4) * batch;
-  dim3 grid(std::min(ntiles, sm_count() * 3));
+  dim3 grid(std::min(ntiles, sm_count() * apply_cl_ctas<L0>()));
   const int smem = apply_cl_smem<L0>();
   static bool attr_set = false;
   if (!attr_set) {
