@@ -629,11 +629,12 @@ static fllf_status apply_impl(fllf_plan p, const fllf_apply_args* a, float* d_ou
     }
   }
   for (int i = 0; i < p->KL; ++i) {
-    const float a = ap.a[i];
-    ap.wk[i][0] = make_float2(a, a);
-    ap.wk[i][1] = make_float2(-a / 64.f, -a / 64.f);
-    ap.wk[i][2] = make_float2(-a / 16.f, -a / 16.f);
-    ap.wk[i][3] = make_float2(-a / 4.f, -a / 4.f);
+    // MAPS (Clenshaw kernel): the per-pixel a_k(q) = [m sigma^3 c0 exp(...)](q) * k, the k here
+    const float a = mode == FLLF_MAPS ? (float)(p->kb + i) : ap.a[i];
+    ap.wk[i][0] = make_float2(ap.a[i], ap.a[i]);
+    ap.wk[i][1] = make_float2(-ap.a[i] / 64.f, -ap.a[i] / 64.f);
+    ap.wk[i][2] = make_float2(-ap.a[i] / 16.f, -ap.a[i] / 16.f);
+    ap.wk[i][3] = make_float2(-ap.a[i] / 4.f, -ap.a[i] / 4.f);
     ap.cw[i][0] = make_float2(-a / 64.f, a / 64.f);
     ap.cw[i][1] = make_float2(-a / 16.f, a / 16.f);
     ap.cw[i][2] = make_float2(-a / 4.f, a / 4.f);

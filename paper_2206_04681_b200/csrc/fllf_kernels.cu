@@ -1092,6 +1092,14 @@ constexpr int HDR_D_ROW = 272;
 constexpr int HDR_D_OFF = 8 * HDR_G_ROW;
 constexpr int HDR_BYTES = 5504;  // 8*480 + 6*272 = 5472, rounded to 128
 static_assert(HDR_D_OFF + 6 * HDR_D_ROW <= HDR_BYTES, "tile header layout");
+// MAPS mode: the header also carries the 8 fine rows of the sigma_r and m maps
+// (their Gaussian pyramids at l >= 1, reading R7)
+constexpr int HDR_S_OFF = HDR_BYTES;
+constexpr int HDR_M_OFF = HDR_S_OFF + 8 * HDR_G_ROW;
+template <bool MAPS>
+__host__ __device__ constexpr int hdr_bytes() {
+  return MAPS ? HDR_M_OFF + 8 * HDR_G_ROW : HDR_BYTES;  // 13184 = 103 x 128
+}
 
 // Orders per ring stage (level 0: two, which halves the barrier and index
 // bookkeeping per order) and ring depth.
@@ -1109,18 +1117,25 @@ template <bool LEVEL0>
 __host__ __device__ constexpr int apply_cl_ctas() {
   return LEVEL0 ? FLLF_APPLY0_CTAS : 3;
 }
-template <bool LEVEL0>
+template <bool LEVEL0, bool MAPS = false>
 __host__ __device__ constexpr int apply_cl_stages() {
-  return LEVEL0 ? (FLLF_APPLY0_CTAS >= 4 ? 6 : 8) : 5;
+  return LEVEL0 ? (FLLF_APPLY0_CTAS >= 4 ? 6 : 8) : (MAPS ? 4 : 5);
 }
-template <bool LEVEL0>
+template <bool LEVEL0, bool MAPS = false>
 __host__ __device__ constexpr int apply_cl_smem() {
-  return apply_cl_stages<LEVEL0>() * apply_cl_ops<LEVEL0>() * apply_stage_bytes<LEVEL0>() + 2 * HDR_BYTES;
+  return apply_cl_stages<LEVEL0, MAPS>() * apply_cl_ops<LEVEL0>() * apply_stage_bytes<LEVEL0>() + 2 * hdr_bytes<MAPS>();
 }
 
-template <bool LEVEL0, bool HAS_D>
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+template <bool LEVEL0, bool HAS_D, bool MAPS>
 __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0>()) k_apply_cl(const __grid_constant__ ApplyParams P, const int ntiles) {
-  constexpr int S = apply_cl_stages<LEVEL0>();
+  constexpr int S = apply_cl_stages<LEVEL0, MAPS>();
+  constexpr int HB = hdr_bytes<MAPS>();
   constexpr int OPS = apply_cl_ops<LEVEL0>();
   constexpr int OBYTES = apply_stage_bytes<LEVEL0>();  // one order
   constexpr int STAGE = OPS * OBYTES;
@@ -1129,7 +1144,7 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0>()) k_apply_cl(const
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t full[S];
   __shared__ __align__(8) uint64_t empty[S];
-  __shared__ __align__(8) uint64_t gfull[2], dfull[2], hempty[2];
+  __shared__ __align__(8) uint64_t gfull[2], dfull[2], hempty[2], mfull[2];
 
   if (P.wait_first) pdl_wait();
   pdl_trigger();
@@ -1152,6 +1167,7 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0>()) k_apply_cl(const
     for (int b = 0; b < 2; ++b) {
       mbar_init(&gfull[b], 1);
       mbar_init(&dfull[b], 1);
+      mbar_init(&mfull[b], 1);
       mbar_init(&hempty[b], 4);
     }
     fence_mbar_init();
@@ -1171,7 +1187,7 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0>()) k_apply_cl(const
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++nt, it.next()) {
       const ApplyTile T = it.tile();
       const int hb = nt & 1;
-      unsigned char* hdr = smem + HOFF + hb * HDR_BYTES;
+      unsigned char* hdr = smem + HOFF + hb * HB;
       if (nt >= 2) mbar_wait_parity(&hempty[hb], ((nt >> 1) & 1) ^ 1u);
       // interior tiles: the 8 fine g rows / 6 coarse D rows are contiguous -> one tensor copy each
       const bool tmg = P.use_tm_g && 2 * T.r0 + 7 <= min(P.Hf - 1, P.fr_hi);
@@ -1201,6 +1217,34 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0>()) k_apply_cl(const
           for (int q = 0; q < 8; ++q)
             tma_load_1d(hdr + q * HDR_G_ROW, gb + (long long)min(2 * T.r0 + q, P.fr_hi) * gp + 120 * T.jb, gbytes,
                         &gfull[hb]);
+        }
+        __syncwarp();
+      }
+      if (MAPS) {  // sigma_r / m rows (full frame; 16-byte aligned rows, checked by the host)
+        const float* sb;
+        const float* mb;
+        long long mp;
+        int wlim;
+        if (LEVEL0) {
+          sb = P.smap.p;
+          mb = P.mmap.p;
+          mp = P.smap.pitch;
+          wlim = P.Wf;
+        } else {
+          sb = P.fine.MS;
+          mb = P.fine.MM;
+          mp = P.fine.pitch;
+          wlim = P.fine.pitch;
+        }
+        const uint32_t mbytes = (uint32_t)min(HDR_G_ROW, (wlim - 120 * T.jb) * 4);
+        if (elect_one()) {
+          mbar_arrive_expect_tx(&mfull[hb], 16 * mbytes);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const long long ro = (long long)min(2 * T.r0 + q, P.Hf - 1) * mp + 120 * T.jb;
+            tma_load_1d(hdr + HDR_S_OFF + q * HDR_G_ROW, sb + ro, mbytes, &mfull[hb]);
+            tma_load_1d(hdr + HDR_M_OFF + q * HDR_G_ROW, mb + ro, mbytes, &mfull[hb]);
+          }
         }
         __syncwarp();
       }
@@ -1290,7 +1334,7 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0>()) k_apply_cl(const
     const ApplyTile T = it.tile();
     const int hb = nt & 1;
     const uint32_t hph = (nt >> 1) & 1;
-    const unsigned char* hdr = smem + HOFF + hb * HDR_BYTES;
+    const unsigned char* hdr = smem + HOFF + hb * HB;
     const int r = T.r0 + warp;
     const int j = T.jb * 30 + lane - 1;  // coarse columns 2j, 2j+1 -> fine columns 4j..4j+3
     const bool act = r < P.r_end && lane >= 1 && lane <= 30 && 4 * j < P.Wf;
@@ -1319,6 +1363,24 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0>()) k_apply_cl(const
       float c;
       sincos_turns(g[p], P.invT, &sn[p], &c);
       tc[p] = 2.f * c;
+    }
+    // MAPS (Sec. III-B): a_k(p) = m sigma^3 c0 k exp(-k^2 hq sigma^2) = Am[p] k 2^(k^2 Bm[p]);
+    // the factor k sits in P.cw (built with a_k := k), the rest per pixel and order
+    float Am[8], Bm[8];
+    if (MAPS) {
+      mbar_wait_parity(&mfull[hb], hph);
+#pragma unroll
+      for (int tt = 0; tt < 2; ++tt) {
+        const float4 sv = *reinterpret_cast<const float4*>(hdr + HDR_S_OFF + (2 * warp + tt) * HDR_G_ROW + lg * 16);
+        const float4 mv = *reinterpret_cast<const float4*>(hdr + HDR_M_OFF + (2 * warp + tt) * HDR_G_ROW + lg * 16);
+        const float sg[4] = {sv.x, sv.y, sv.z, sv.w}, mm[4] = {mv.x, mv.y, mv.z, mv.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float s2 = sg[q] * sg[q];
+          Am[4 * tt + q] = mm[q] * s2 * sg[q] * P.c0;
+          Bm[4 * tt + q] = -P.hq * 1.4426950408889634f * s2;
+        }
+      }
     }
     float2 b1[8], b2[8];
 #pragma unroll
@@ -1355,13 +1417,28 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0>()) k_apply_cl(const
       raw[6] = pfma(bc(6.f), vob, padd(voa, Ro));
       raw[7] = padd(vob, Ro);
       const float2 w64 = P.cw[i][0], w16 = P.cw[i][1], w4 = P.cw[i][2];
+      float kk2 = 0.f;
+      if (MAPS) {
+        const float kk = (float)(P.kbase + i);
+        kk2 = kk * kk;
+      }
 #pragma unroll
       for (int p = 0; p < 8; ++p) {
         const float2 w = (p < 4) ? ((p & 1) ? w16 : w64) : ((p & 1) ? w4 : w16);
-        float2 c = pfma(raw[p], w, pneg(bn[p]));
-        if (!LEVEL0) {
-          const float4 fv = fz[(p >> 2) * 2 + ((p & 3) >> 1)];
-          c = pfma((p & 1) ? hi2(fv) : lo2(fv), P.cw[i][3], c);
+        float2 c;
+        if (MAPS) {
+          c = pmul(raw[p], w);
+          if (!LEVEL0) {
+            const float4 fv = fz[(p >> 2) * 2 + ((p & 3) >> 1)];
+            c = pfma((p & 1) ? hi2(fv) : lo2(fv), P.cw[i][3], c);
+          }
+          c = pfma(c, bc(Am[p] * ex2_approx(kk2 * Bm[p])), pneg(bn[p]));
+        } else {
+          c = pfma(raw[p], w, pneg(bn[p]));
+          if (!LEVEL0) {
+            const float4 fv = fz[(p >> 2) * 2 + ((p & 3) >> 1)];
+            c = pfma((p & 1) ? hi2(fv) : lo2(fv), P.cw[i][3], c);
+          }
         }
         bn[p] = pfma(bc(tc[p]), bp[p], c);
       }
@@ -1645,18 +1722,18 @@ static cudaError_t launch_apply_t(const ApplyParams& p, int batch, cudaStream_t 
   return launch_ex(k_apply<L0, HD, MP>, grid, dim3(160), smem, s, pdl, p, ntiles);
 }
 
-template <bool L0, bool HD>
+template <bool L0, bool HD, bool MP>
 static cudaError_t launch_apply_cl_t(const ApplyParams& p, int batch, cudaStream_t s, bool pdl) {
   const int ntiles = ((p.Wf + 119) / 120) * ((p.r_end - p.r_begin + 3) / 4) * batch;
   dim3 grid(std::min(ntiles, sm_count() * apply_cl_ctas<L0>()));
-  const int smem = apply_cl_smem<L0>();
+  const int smem = apply_cl_smem<L0, MP>();
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_apply_cl<L0, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(k_apply_cl<L0, HD, MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  return launch_ex(k_apply_cl<L0, HD>, grid, dim3(160), smem, s, pdl, p, ntiles);
+  return launch_ex(k_apply_cl<L0, HD, MP>, grid, dim3(160), smem, s, pdl, p, ntiles);
 }
 
 cudaError_t launch_apply(const ApplyParams& p, int level_fine, bool has_d, bool maps, int batch,
@@ -1665,13 +1742,24 @@ cudaError_t launch_apply(const ApplyParams& p, int level_fine, bool has_d, bool 
     const char* e = std::getenv("FLLF_APPLY_V1");
     return e && e[0] == '1';
   }();
-  if (!maps && !v1) {
+  // MAPS through the Clenshaw kernel when the level-0 maps can be staged by
+  // bulk copies (16-byte aligned rows, W a multiple of 4); else the forward kernel
+  const bool maps_cl = maps && (((reinterpret_cast<uintptr_t>(p.smap.p) | reinterpret_cast<uintptr_t>(p.mmap.p)) & 15) == 0) &&
+                       ((p.smap.pitch & 3) == 0) && ((p.mmap.pitch & 3) == 0) && (p.smap.pitch == p.mmap.pitch) &&
+                       ((p.img.W & 3) == 0);
+  static const bool maps_v1 = [] {
+    const char* e = std::getenv("FLLF_MAPS_V1");
+    return e && e[0] == '1';
+  }();
+  if (!v1 && (!maps || (maps_cl && !maps_v1))) {
+#define FLLF_CL(L0, HD) return maps ? launch_apply_cl_t<L0, HD, true>(p, batch, s, pdl) : launch_apply_cl_t<L0, HD, false>(p, batch, s, pdl)
     if (level_fine == 0) {
-      if (has_d) return launch_apply_cl_t<true, true>(p, batch, s, pdl);
-      return launch_apply_cl_t<true, false>(p, batch, s, pdl);
+      if (has_d) FLLF_CL(true, true);
+      FLLF_CL(true, false);
     }
-    if (has_d) return launch_apply_cl_t<false, true>(p, batch, s, pdl);
-    return launch_apply_cl_t<false, false>(p, batch, s, pdl);
+    if (has_d) FLLF_CL(false, true);
+    FLLF_CL(false, false);
+#undef FLLF_CL
   }
 #define FLLF_APPLY(L0, HD, MP) return launch_apply_t<L0, HD, MP>(p, batch, s, pdl)
   if (level_fine == 0) {
