@@ -29,12 +29,13 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def build(verbose: bool = False, extra: list[str] | None = None) -> str:
+def build(verbose: bool = False, extra: list[str] | None = None, out: str | None = None) -> str:
     os.makedirs(LIBDIR, exist_ok=True)
+    lib = out or LIB
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
            "-Xcompiler", "-fvisibility=hidden", "-I", INCLUDE, "-I", CSRC,
-           "-Xptxas", "-v" if verbose else "-O3", *srcs, "-o", LIB, *(extra or [])]
+           "-Xptxas", "-v" if verbose else "-O3", *srcs, "-o", lib, *(extra or [])]
     # export only the C ABI (fllf_*): visibility=hidden + explicit default visibility
     cmd += ["-DFLLF_BUILD"]
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -43,8 +44,16 @@ def build(verbose: bool = False, extra: list[str] | None = None) -> str:
         raise RuntimeError("nvcc failed building libfllf.so")
     if verbose:
         sys.stderr.write(r.stderr)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv))
+    # python -m paper_2206_04681_b200.build [-v] [--variant NAME -DMACRO=V ...]: variants go to
+    # lib/variants/libfllf_NAME.so (select with FLLF_LIB=...) for compile-time A/B runs
+    if "--variant" in sys.argv:
+        i = sys.argv.index("--variant")
+        name, defs = sys.argv[i + 1], [a for a in sys.argv[i + 2:] if a.startswith("-D")]
+        os.makedirs(os.path.join(LIBDIR, "variants"), exist_ok=True)
+        print(build(extra=defs, out=os.path.join(LIBDIR, "variants", f"libfllf_{name}.so")))
+    else:
+        print(build(verbose="-v" in sys.argv))

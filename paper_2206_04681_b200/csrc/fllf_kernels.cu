@@ -654,7 +654,10 @@ struct Build0Warp {
 };
 
 template <int NC>
-__global__ void __launch_bounds__(32, 16) k_build0(const BuildParams P) {
+#ifndef FLLF_B0_MINB
+#define FLLF_B0_MINB 16
+#endif
+__global__ void __launch_bounds__(32, FLLF_B0_MINB) k_build0(const BuildParams P) {
   pdl_trigger();
   const int cb = blockIdx.x;
   if (cb * 30 >= P.Wc) return;

@@ -16,7 +16,8 @@ from dataclasses import dataclass
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libfllf.so")
+# FLLF_LIB selects another build of the same library (compile-time A/B of kernel variants)
+LIB_PATH = os.environ.get("FLLF_LIB") or os.path.join(_PKG, "lib", "libfllf.so")
 HEADER_PATH = os.path.join(os.path.dirname(_PKG), "include", "fllf.h")
 
 FLLF_OK = 0
