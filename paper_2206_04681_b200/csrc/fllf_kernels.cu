@@ -1650,11 +1650,7 @@ cudaError_t launch_build(const BuildParams& p0, int level_src, int batch, cudaSt
     if (level_src == 0) return launch_ex(k_build<0, 2, true, false>, grid, dim3(32), 0, s, pdl, p);
     return launch_ex(k_build<0, 2, false, false>, grid, dim3(32), 0, s, pdl, p);
   }
-  static const bool b0v1 = [] {
-    const char* e = std::getenv("FLLF_BUILD0_V1");
-    return e && e[0] == '1';  // FLLF_BUILD0_V1=1: the previous level-0 build (A/B only)
-  }();
-  if (level_src == 0 && !b0v1) {
+  if (level_src == 0) {
     static const int cap = [] {
       const char* e = std::getenv("FLLF_BUILD0V2_CHUNK");
       const int v = e ? std::atoi(e) : 8;
@@ -1669,23 +1665,6 @@ cudaError_t launch_build(const BuildParams& p0, int level_src, int batch, cudaSt
       case 3: return launch_build0_nc<3>(p, batch, s, pdl);
       case 2: return launch_build0_nc<2>(p, batch, s, pdl);
       default: return launch_build0_nc<1>(p, batch, s, pdl);
-    }
-  }
-  if (level_src == 0) {
-    static const int cap0 = [] {
-      const char* e = std::getenv("FLLF_BUILD0_CHUNK");
-      const int v = e ? std::atoi(e) : 4;  // measured best on B200
-      return v >= 1 && v <= 8 ? v : 4;
-    }();
-    switch (chunk_for(p.KL, cap0)) {
-      case 8: return launch_build_nc<8, true>(p, batch, s, pdl);
-      case 7: return launch_build_nc<7, true>(p, batch, s, pdl);
-      case 6: return launch_build_nc<6, true>(p, batch, s, pdl);
-      case 5: return launch_build_nc<5, true>(p, batch, s, pdl);
-      case 4: return launch_build_nc<4, true>(p, batch, s, pdl);
-      case 3: return launch_build_nc<3, true>(p, batch, s, pdl);
-      case 2: return launch_build_nc<2, true>(p, batch, s, pdl);
-      default: return launch_build_nc<1, true>(p, batch, s, pdl);
     }
   }
   static const int cap1 = [] {
@@ -1741,10 +1720,6 @@ static cudaError_t launch_apply_cl_t(const ApplyParams& p, int batch, cudaStream
 
 cudaError_t launch_apply(const ApplyParams& p, int level_fine, bool has_d, bool maps, int batch,
                          cudaStream_t s, bool pdl) {
-  static const bool v1 = [] {
-    const char* e = std::getenv("FLLF_APPLY_V1");
-    return e && e[0] == '1';
-  }();
   // MAPS through the Clenshaw kernel when the level-0 maps can be staged by
   // bulk copies (16-byte aligned rows, W a multiple of 4); else the forward kernel
   const bool maps_cl = maps && (((reinterpret_cast<uintptr_t>(p.smap.p) | reinterpret_cast<uintptr_t>(p.mmap.p)) & 15) == 0) &&
@@ -1754,7 +1729,7 @@ cudaError_t launch_apply(const ApplyParams& p, int level_fine, bool has_d, bool 
     const char* e = std::getenv("FLLF_MAPS_V1");
     return e && e[0] == '1';
   }();
-  if (!v1 && (!maps || (maps_cl && !maps_v1))) {
+  if (!maps || (maps_cl && !maps_v1)) {
 #define FLLF_CL(L0, HD) return maps ? launch_apply_cl_t<L0, HD, true>(p, batch, s, pdl) : launch_apply_cl_t<L0, HD, false>(p, batch, s, pdl)
     if (level_fine == 0) {
       if (has_d) FLLF_CL(true, true);
