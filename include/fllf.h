@@ -153,6 +153,24 @@ FLLF_API fllf_status fllf_filter(fllf_plan p, const float* d_img, size_t in_pitc
  * Asynchronous on `s` (pinned host memory); synchronise `s` before reading h_out. */
 FLLF_API fllf_status fllf_filter_host(fllf_plan p, const float* h_img, float* h_out, void* s);
 
+/* Streaming end-to-end from HOST memory: nframes successive batches (each the
+ * plan's B frames of H*W floats, dense W*4 pitch), batch i read from
+ * h_in + i*in_stride_bytes and written to h_out + i*out_stride_bytes (a
+ * stride of 0 reuses one buffer).  Three-stage pipeline on two internal copy
+ * streams and `s`: the H2D copy of batch i+1 and the D2H copy of batch i-1
+ * overlap the filter of batch i (double-buffered device staging owned by the
+ * plan).  Asynchronous: `s` completes after the last result has reached the
+ * host; work queued on `s` before the call is ordered before the first copy.
+ * Host memory must be pinned for the copies to overlap.  Not for row-band
+ * plans or inside a stream capture (FLLF_ERR_INVALID_ARGUMENT). */
+FLLF_API fllf_status fllf_filter_host_frames(fllf_plan p, const float* h_in, size_t in_stride_bytes, float* h_out,
+                                             size_t out_stride_bytes, int nframes, void* s);
+
+/* Bench tooling: with a device buffer set, fllf_filter_host_frames writes it
+ * (cudaMemsetAsync on `s`, inside the pipeline) before each batch's filter,
+ * evicting the previous batch's data from L2.  bytes = 0 disables. */
+FLLF_API fllf_status fllf_plan_set_l2_flush(fllf_plan p, void* d_buf, size_t bytes);
+
 /* Host helper: omega_k and a_k = m alpha~_k for k = 1..K in fp64 (Eq. 9-11). */
 FLLF_API fllf_status fllf_coefficients(int K, double T, double sigma_r, double m, double* omega_out,
                               double* a_out);

@@ -90,13 +90,27 @@ struct fllf_plan_s {
   bool use_pdl = true;  // programmatic dependent launch between the kernels of a sequence
   bool capturing = false;
   cudaStream_t cap_stream = nullptr;
-  cudaGraphExec_t gexec = nullptr;
-  const void* g_in = nullptr;
-  const void* g_out = nullptr;
-  size_t g_in_pitch = 0, g_out_pitch = 0;
-  bool g_prof = false;
-  int g_launches = 0;
-  int g_nrec = 0;
+  struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    const void* in = nullptr;
+    const void* out = nullptr;
+    size_t in_pitch = 0, out_pitch = 0;
+    bool prof = false;
+    int launches = 0;
+    int nrec = 0;
+    unsigned long long used = 0;  // LRU stamp
+  };
+  static constexpr int kGraphCache = 4;  // buffer pairs (fllf_filter_host_frames alternates two)
+  GraphEntry graphs[kGraphCache];
+  unsigned long long graph_clock = 0;
+  // fllf_filter_host_frames: double-buffered device staging and the copy streams
+  float* pipe_in[2] = {nullptr, nullptr};
+  float* pipe_out[2] = {nullptr, nullptr};
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev_pstart = nullptr, ev_pend = nullptr;
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
+  void* flush_buf = nullptr;  // bench tooling: L2 flush between pipelined frames
+  size_t flush_bytes = 0;
   // TMA descriptors of each level's Z planes (k_apply_cl): as the coarse
   // level (box 128 floats x 6 rows) and as the fine level (box 256 x 8)
   bool tm_ok = false;
@@ -415,7 +429,18 @@ fllf_status fllf_destroy(fllf_plan p) {
     if (p->stage_out) cudaFree(p->stage_out);
     for (cudaEvent_t e : p->ev_start) cudaEventDestroy(e);
     for (cudaEvent_t e : p->ev_stop) cudaEventDestroy(e);
-    if (p->gexec) cudaGraphExecDestroy(p->gexec);
+    for (auto& g : p->graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+    for (int i = 0; i < 2; ++i) {
+      if (p->pipe_in[i]) cudaFree(p->pipe_in[i]);
+      if (p->pipe_out[i]) cudaFree(p->pipe_out[i]);
+      for (cudaEvent_t ev : {p->ev_in[i], p->ev_done[i], p->ev_out[i]})
+        if (ev) cudaEventDestroy(ev);
+    }
+    if (p->s_h2d) cudaStreamDestroy(p->s_h2d);
+    if (p->s_d2h) cudaStreamDestroy(p->s_d2h);
+    if (p->ev_pstart) cudaEventDestroy(p->ev_pstart);
+    if (p->ev_pend) cudaEventDestroy(p->ev_pend);
     if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
     cudaGetLastError();
   }
@@ -749,12 +774,23 @@ fllf_status fllf_filter(fllf_plan p, const float* d_img, size_t in_pitch_bytes, 
   if (!p) return fail(FLLF_ERR_BAD_POINTER, "NULL plan");
   if (!p->use_graph) return filter_eager(p, d_img, in_pitch_bytes, d_out, out_pitch_bytes, s);
   DeviceGuard guard(p->device);
-  const bool hit = p->gexec && p->g_in == d_img && p->g_out == d_out && p->g_in_pitch == in_pitch_bytes &&
-                   p->g_out_pitch == out_pitch_bytes && p->g_prof == p->profiling;
-  if (!hit) {
-    if (p->gexec) {
-      cudaGraphExecDestroy(p->gexec);
-      p->gexec = nullptr;
+  fllf_plan_s::GraphEntry* g = nullptr;
+  for (auto& c : p->graphs)
+    if (c.exec && c.in == d_img && c.out == d_out && c.in_pitch == in_pitch_bytes && c.out_pitch == out_pitch_bytes &&
+        c.prof == p->profiling)
+      g = &c;
+  if (!g) {
+    g = &p->graphs[0];  // an empty slot, else the least recently used one
+    for (auto& c : p->graphs) {
+      if (!c.exec) {
+        g = &c;
+        break;
+      }
+      if (c.used < g->used) g = &c;
+    }
+    if (g->exec) {
+      cudaGraphExecDestroy(g->exec);
+      g->exec = nullptr;
     }
     if (!p->cap_stream) {
       cudaError_t e = cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking);
@@ -772,29 +808,30 @@ fllf_status fllf_filter(fllf_plan p, const float* d_img, size_t in_pitch_bytes, 
       return st;
     }
     if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
-    e = cudaGraphInstantiate(&p->gexec, graph, 0);
+    e = cudaGraphInstantiate(&g->exec, graph, 0);
     cudaGraphDestroy(graph);
     if (e != cudaSuccess) {
-      p->gexec = nullptr;
+      g->exec = nullptr;
       return cuda_fail(e, "cudaGraphInstantiate");
     }
-    p->g_in = d_img;
-    p->g_out = d_out;
-    p->g_in_pitch = in_pitch_bytes;
-    p->g_out_pitch = out_pitch_bytes;
-    p->g_prof = p->profiling;
-    p->g_launches = p->last_launches;
-    p->g_nrec = p->nrec;
+    g->in = d_img;
+    g->out = d_out;
+    g->in_pitch = in_pitch_bytes;
+    g->out_pitch = out_pitch_bytes;
+    g->prof = p->profiling;
+    g->launches = p->last_launches;
+    g->nrec = p->nrec;
   }
-  cudaError_t e = cudaGraphLaunch(p->gexec, static_cast<cudaStream_t>(s));
+  g->used = ++p->graph_clock;
+  cudaError_t e = cudaGraphLaunch(g->exec, static_cast<cudaStream_t>(s));
   if (e != cudaSuccess) return cuda_fail(e, "cudaGraphLaunch");
   // the replay leaves the plan in the state of a fresh build + apply
   p->built = true;
   p->img = d_img;
   p->img_pitch = (long long)((in_pitch_bytes ? in_pitch_bytes : (size_t)p->d.W * 4) / 4);
   p->last_was_apply = true;
-  p->last_launches = p->g_launches;
-  p->nrec = p->g_nrec;
+  p->last_launches = g->launches;
+  p->nrec = g->nrec;
   return FLLF_OK;
 }
 
@@ -816,6 +853,83 @@ fllf_status fllf_filter_host(fllf_plan p, const float* h_img, float* h_out, void
   if (st != FLLF_OK) return st;
   e = cudaMemcpyAsync(h_out, p->stage_out, bytes, cudaMemcpyDeviceToHost, stream);
   if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
+  return FLLF_OK;
+}
+
+static fllf_status pipe_setup(fllf_plan p, size_t bytes) {
+  if (p->pipe_in[0]) return FLLF_OK;
+  for (int i = 0; i < 2; ++i) {
+    if (cudaMalloc(&p->pipe_in[i], bytes) != cudaSuccess || cudaMalloc(&p->pipe_out[i], bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(FLLF_ERR_OUT_OF_MEMORY, "filter_host_frames: staging cudaMalloc failed");
+    }
+  }
+  cudaError_t e = cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking);
+  cudaEvent_t* evs[] = {&p->ev_pstart, &p->ev_pend, &p->ev_in[0], &p->ev_in[1], &p->ev_done[0], &p->ev_done[1],
+                        &p->ev_out[0], &p->ev_out[1]};
+  for (cudaEvent_t* ev : evs)
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+  return e == cudaSuccess ? FLLF_OK : cuda_fail(e, "filter_host_frames: stream / event creation");
+}
+
+fllf_status fllf_filter_host_frames(fllf_plan p, const float* h_in, size_t in_stride_bytes, float* h_out,
+                                    size_t out_stride_bytes, int nframes, void* s) {
+  if (!p) return fail(FLLF_ERR_BAD_POINTER, "NULL plan");
+  if (!h_in || !h_out) return fail(FLLF_ERR_BAD_POINTER, "filter_host_frames: NULL host pointer");
+  if (nframes < 0) return fail(FLLF_ERR_INVALID_ARGUMENT, "filter_host_frames: nframes < 0");
+  if (p->band) return fail(FLLF_ERR_INVALID_ARGUMENT, "filter_host_frames: not for row-band plans");
+  if (p->capturing) return fail(FLLF_ERR_INVALID_ARGUMENT, "filter_host_frames: not inside a stream capture");
+  if (nframes == 0) return FLLF_OK;
+  DeviceGuard guard(p->device);
+  const size_t bytes = (size_t)p->d.batch * p->d.H * p->d.W * sizeof(float);
+  fllf_status st = pipe_setup(p, bytes);
+  if (st != FLLF_OK) return st;
+  cudaStream_t cs = static_cast<cudaStream_t>(s);
+  const char* hi = reinterpret_cast<const char*>(h_in);
+  char* ho = reinterpret_cast<char*>(h_out);
+  // the copies start after the work already queued on s
+  cudaError_t e = cudaEventRecord(p->ev_pstart, cs);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(p->s_h2d, p->ev_pstart, 0);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(p->s_d2h, p->ev_pstart, 0);
+  if (e != cudaSuccess) return cuda_fail(e, "filter_host_frames: fork");
+  int launches = 0;
+  for (int i = 0; i < nframes; ++i) {
+    const int b = i & 1;
+    // H2D of frame i into slot b once frame i-2's build has read it
+    if (i >= 2) e = cudaStreamWaitEvent(p->s_h2d, p->ev_done[b], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(p->pipe_in[b], hi + (size_t)i * in_stride_bytes, bytes, cudaMemcpyHostToDevice, p->s_h2d);
+    if (e == cudaSuccess) e = cudaEventRecord(p->ev_in[b], p->s_h2d);
+    // filter on s once the input has landed and frame i-2's result has left slot b
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, p->ev_in[b], 0);
+    if (e == cudaSuccess && i >= 2) e = cudaStreamWaitEvent(cs, p->ev_out[b], 0);
+    if (e == cudaSuccess && p->flush_buf) e = cudaMemsetAsync(p->flush_buf, i & 0xff, p->flush_bytes, cs);
+    if (e != cudaSuccess) return cuda_fail(e, "filter_host_frames: H2D stage");
+    st = fllf_filter(p, p->pipe_in[b], 0, p->pipe_out[b], 0, s);
+    if (st != FLLF_OK) return st;
+    launches += p->last_launches;
+    e = cudaEventRecord(p->ev_done[b], cs);
+    // D2H of frame i's result
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(p->s_d2h, p->ev_done[b], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(ho + (size_t)i * out_stride_bytes, p->pipe_out[b], bytes, cudaMemcpyDeviceToHost, p->s_d2h);
+    if (e == cudaSuccess) e = cudaEventRecord(p->ev_out[b], p->s_d2h);
+    if (e != cudaSuccess) return cuda_fail(e, "filter_host_frames: D2H stage");
+  }
+  // join: s completes after the last result has reached the host
+  e = cudaEventRecord(p->ev_pend, p->s_d2h);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, p->ev_pend, 0);
+  if (e != cudaSuccess) return cuda_fail(e, "filter_host_frames: join");
+  p->last_launches = launches;
+  return FLLF_OK;
+}
+
+fllf_status fllf_plan_set_l2_flush(fllf_plan p, void* d_buf, size_t bytes) {
+  if (!p) return fail(FLLF_ERR_BAD_POINTER, "NULL plan");
+  if (!d_buf && bytes) return fail(FLLF_ERR_BAD_POINTER, "set_l2_flush: NULL buffer");
+  p->flush_buf = bytes ? d_buf : nullptr;
+  p->flush_bytes = bytes;
   return FLLF_OK;
 }
 

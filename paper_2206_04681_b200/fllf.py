@@ -68,6 +68,8 @@ _SIGS = {
     "fllf_apply": (ctypes.c_int, [_P, ctypes.POINTER(fllf_apply_args), _P, ctypes.c_size_t, _P]),
     "fllf_filter": (ctypes.c_int, [_P, _P, ctypes.c_size_t, _P, ctypes.c_size_t, _P]),
     "fllf_filter_host": (ctypes.c_int, [_P, _P, _P, _P]),
+    "fllf_filter_host_frames": (ctypes.c_int, [_P, _P, ctypes.c_size_t, _P, ctypes.c_size_t, ctypes.c_int, _P]),
+    "fllf_plan_set_l2_flush": (ctypes.c_int, [_P, _P, ctypes.c_size_t]),
     "fllf_coefficients": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, ctypes.c_double,
                                          ctypes.c_double, ctypes.POINTER(ctypes.c_double),
                                          ctypes.POINTER(ctypes.c_double)]),
@@ -304,6 +306,28 @@ def fllf_filter_host(plan, h_img, h_out, stream=None) -> None:
         if t.is_cuda or not t.is_contiguous():
             raise TypeError(f"{n} must be a contiguous host tensor")
     _check(lib.fllf_filter_host(plan, h_img.data_ptr(), h_out.data_ptr(), _stream_handle(stream)))
+
+
+def fllf_filter_host_frames(plan, h_in, in_stride_bytes, h_out, out_stride_bytes, nframes, stream=None) -> None:
+    """Streaming host -> device -> host over `nframes` batches (C: fllf_filter_host_frames).
+    h_in / h_out: contiguous float32 CPU tensors (pinned for overlap) holding the
+    batches at the given byte strides (0 = one buffer reused for every batch)."""
+    for t, n in ((h_in, "h_in"), (h_out, "h_out")):
+        if t.is_cuda or not t.is_contiguous():
+            raise TypeError(f"{n} must be a contiguous host tensor")
+    for t, st, n in ((h_in, in_stride_bytes, "h_in"), (h_out, out_stride_bytes, "h_out")):
+        if nframes > 0 and (nframes - 1) * st + 1 > t.numel() * 4:
+            raise ValueError(f"{n} too small for {nframes} batches at stride {st}")
+    _check(lib.fllf_filter_host_frames(plan, h_in.data_ptr(), int(in_stride_bytes), h_out.data_ptr(),
+                                       int(out_stride_bytes), int(nframes), _stream_handle(stream)))
+
+
+def fllf_plan_set_l2_flush(plan, buf=None) -> None:
+    """Bench tooling: a CUDA tensor written before each batch of fllf_filter_host_frames (None: off)."""
+    if buf is None:
+        _check(lib.fllf_plan_set_l2_flush(plan, None, 0))
+    else:
+        _check(lib.fllf_plan_set_l2_flush(plan, buf.data_ptr(), buf.numel() * buf.element_size()))
 
 
 def fllf_coefficients(K, T, sigma_r, m):

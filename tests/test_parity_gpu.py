@@ -187,6 +187,28 @@ def test_filter_host_path(F):
     assert maxerr(h_out.numpy(), ref) <= TOL_OUT
 
 
+@pytest.mark.parametrize("nb,batch", [(1, 1), (5, 1), (4, 2)])
+def test_filter_host_frames_stream(F, nb, batch):
+    """Streaming host path: nb batches through the double-buffered pipeline
+    (odd counts end on either slot), each batch compared with the oracle;
+    the in-pipeline L2 flush is switched on for one case."""
+    H, W, lev, K = 45, 70, 4, 6
+    frames = np.stack([synth.uniform_image(H, W, seed=300 + i) for i in range(nb * batch)]).astype(np.float32)
+    h_in = torch.from_numpy(frames).pin_memory()
+    h_out = torch.full_like(h_in, float("nan")).pin_memory()
+    stride = batch * H * W * 4
+    flush = torch.empty(1 << 20, device="cuda") if nb == 5 else None
+    with F.Plan(H, W, lev, K, 510.0, 30.0, 3.0, batch=batch) as p:
+        F.fllf_plan_set_l2_flush(p.handle, flush)
+        F.fllf_filter_host_frames(p.handle, h_in, stride, h_out, stride, nb)
+        torch.cuda.synchronize()
+        with pytest.raises(F.FllfError):
+            F.fllf_filter_host_frames(p.handle, h_in, stride, h_out, stride, -1)
+    for i in range(nb * batch):
+        ref = O.fourier_llf(frames[i].astype(np.float64), lev, K, 510.0, 30.0, 3.0)
+        assert maxerr(h_out[i].numpy(), ref) <= TOL_OUT
+
+
 def test_error_paths(F):
     with F.Plan(64, 64, 3, 4) as p:
         o = torch.empty((64, 64), device="cuda")
