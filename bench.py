@@ -418,7 +418,7 @@ def run_sharded(args, c, wl, world, rank, local):
     stream = torch.cuda.current_stream()
     for _ in range(max(args.warmup, 1)):
         flush_buf.zero_()
-        D.sharded_filter(fn, out, 3, K)
+        D.sharded_filter(fn, out, 3, K, batch_channels=True)
     torch.cuda.synchronize()
     dist.barrier()
     clk = ClockSampler(local)
@@ -429,7 +429,7 @@ def run_sharded(args, c, wl, world, rank, local):
     for i in range(args.steps):
         flush_buf.zero_()
         starts[i].record(stream)
-        D.sharded_filter(fn, out, 3, K)
+        D.sharded_filter(fn, out, 3, K, batch_channels=True)
         ends[i].record(stream)
         launches += sum(p.launches for p in fn.plans.values())
     torch.cuda.synchronize()

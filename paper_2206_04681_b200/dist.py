@@ -40,6 +40,7 @@ class Segment:
     k_begin: int      # 1-based, inclusive
     k_end: int        # exclusive
     include_base: bool
+    nch: int = 1      # channels channel .. channel+nch-1 with this order range (batch_channels)
 
 
 def order_partition(channels: int, K: int, world: int) -> List[List[Segment]]:
@@ -61,14 +62,32 @@ def order_partition(channels: int, K: int, world: int) -> List[List[Segment]]:
     return out
 
 
+def channel_runs(segs: List[Segment]) -> List[Segment]:
+    """Merge consecutive channels that carry the same order range into one
+    segment with nch > 1 (one batched plan instead of one plan per channel)."""
+    runs: List[Segment] = []
+    for s in sorted(segs, key=lambda x: x.channel):
+        r = runs[-1] if runs else None
+        if (r is not None and r.channel + r.nch == s.channel and (r.k_begin, r.k_end, r.include_base) ==
+                (s.k_begin, s.k_end, s.include_base)):
+            runs[-1] = Segment(r.channel, r.k_begin, r.k_end, r.include_base, r.nch + s.nch)
+        else:
+            runs.append(s)
+    return runs
+
+
 def sharded_filter(partial_fn: Callable, out, channels: int, K: int, group=None, dst: int = 0,
-                   overlap: bool = True):
+                   overlap: bool = True, batch_channels: bool = False):
     """Order-sharded Fourier LLF with one reduce per channel.
 
     partial_fn(segment, out_channel) must write this rank's partial output of
     `segment` INTO out_channel (a (H, W) view of `out`); channels this rank
     has no unit of are zero-filled here.  `out` is (channels, H, W) on the
     rank's device; after the call, rank `dst` holds the full output.
+    batch_channels: consecutive channels with the same order range go to
+    partial_fn as ONE segment (nch > 1) with the (nch, H, W) view -- e.g. all
+    three channels on a single rank as one batched plan; each channel's
+    reduce is issued once its run is computed.
     Returns the list of async work handles already waited on.
     """
     import torch.distributed as dist
@@ -76,6 +95,22 @@ def sharded_filter(partial_fn: Callable, out, channels: int, K: int, group=None,
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     mine = order_partition(channels, K, world)[rank]
+    if batch_channels:
+        runs = channel_runs(mine)
+        done = set()
+        works = []
+        for r in runs:
+            partial_fn(r, out[r.channel:r.channel + r.nch])
+            done.update(range(r.channel, r.channel + r.nch))
+        for c in range(channels):
+            if c not in done:
+                out[c].zero_()
+            w = dist.reduce(out[c], dst=dst, op=dist.ReduceOp.SUM, group=group, async_op=overlap)
+            if overlap:
+                works.append(w)
+        for w in works:
+            w.wait()
+        return works
     by_ch = {}
     for s in mine:
         by_ch.setdefault(s.channel, []).append(s)
@@ -106,13 +141,14 @@ def gpu_partial_fn(img, levels: int, K: int, T: float, sigma_r: float, m: float)
     plans = {}
 
     def fn(seg: Segment, out_c):
-        key = (seg.channel, seg.k_begin, seg.k_end, seg.include_base)
+        key = (seg.channel, seg.k_begin, seg.k_end, seg.include_base, seg.nch)
         p = plans.get(key)
         if p is None:
             p = F.Plan(H, W, levels, K, T, sigma_r, m, k_begin=seg.k_begin, k_end=seg.k_end,
-                       include_base=seg.include_base)
+                       include_base=seg.include_base, batch=seg.nch)
             plans[key] = p
-        p.filter(img[seg.channel], out_c)
+        src = img[seg.channel] if seg.nch == 1 and out_c.dim() == 2 else img[seg.channel:seg.channel + seg.nch]
+        p.filter(src, out_c)
 
     fn.plans = plans
     return fn

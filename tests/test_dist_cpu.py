@@ -61,21 +61,27 @@ def _worker(rank, world, port, img, args, result_path):
     C, H, W = img.shape
     out = torch.zeros((C, H, W), dtype=torch.float64)
 
-    def partial_fn(seg: Segment, out_c):
-        part = O.fourier_llf(img[seg.channel], levels, K, T, sig, m, k_range=(seg.k_begin, seg.k_end),
-                             include_base=False)
-        if seg.include_base:
-            part = part + img[seg.channel]
-        out_c.copy_(torch.from_numpy(part))
+    batch = world == 1 or os.environ.get("FLLF_TEST_BATCH_CH") == "1"
 
-    sharded_filter(partial_fn, out, C, K)
+    def partial_fn(seg: Segment, out_c):
+        views = out_c if batch else out_c[None]
+        assert views.shape[0] == seg.nch and (batch or seg.nch == 1)
+        for i in range(seg.nch):
+            c = seg.channel + i
+            part = O.fourier_llf(img[c], levels, K, T, sig, m, k_range=(seg.k_begin, seg.k_end),
+                                 include_base=False)
+            if seg.include_base:
+                part = part + img[c]
+            views[i].copy_(torch.from_numpy(part))
+
+    sharded_filter(partial_fn, out, C, K, batch_channels=batch)
     if rank == 0:
         np.save(result_path, out.numpy())
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
+@pytest.mark.parametrize("world", [1, 2])
 def test_sharded_filter_gloo_equals_full(tmp_path, world):
     rng = np.random.default_rng(3)
     img = rng.uniform(0, 255, (3, 24, 21))
@@ -85,6 +91,20 @@ def test_sharded_filter_gloo_equals_full(tmp_path, world):
     from oracle import fllf_oracle as O
     full = np.stack([O.fourier_llf(img[c], *args) for c in range(3)])
     assert np.abs(np.load(res) - full).max() <= 1e-9
+
+
+def test_channel_runs():
+    from paper_2206_04681_b200.dist import channel_runs
+    for C, K, world in [(3, 10, 1), (3, 10, 2), (3, 10, 3), (3, 10, 8), (4, 6, 3), (5, 4, 2)]:
+        parts = order_partition(C, K, world)
+        for segs in parts:
+            runs = channel_runs(segs)
+            # same units, channels covered once, merged runs share one order range
+            cov = [c for r in runs for c in range(r.channel, r.channel + r.nch)]
+            assert sorted(cov) == sorted(s.channel for s in segs)
+            for r in runs:
+                assert any(s.channel == r.channel and (s.k_begin, s.k_end) == (r.k_begin, r.k_end) for s in segs)
+    assert [r.nch for r in channel_runs(order_partition(3, 10, 1)[0])] == [3]
 
 
 # ---------------------------------------------------------------- NEXT-1

@@ -176,6 +176,30 @@ def test_batch_equals_frames(F):
         assert maxerr(outb[i], ref) <= TOL_OUT
 
 
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_gpu_partial_fn_channel_runs(F, world):
+    """Config-3 order sharding through dist.gpu_partial_fn with batched channel
+    runs (one plan per run of channels sharing an order range): the ranks'
+    partials, summed as the NCCL reduce would, equal the full oracle per channel."""
+    from paper_2206_04681_b200 import dist as D
+    C, H, W, lev, K = 3, 40, 58, 4, 5
+    rgb = np.stack([synth.uniform_image(H, W, seed=400 + c) for c in range(C)]).astype(np.float32)
+    img = torch.from_numpy(rgb).cuda()
+    total = torch.zeros((C, H, W), dtype=torch.float64)
+    for segs in D.order_partition(C, K, world):
+        fn = D.gpu_partial_fn(img, lev, K, 510.0, 20.0, 2.0)
+        out = torch.zeros((C, H, W), device="cuda")
+        for r in D.channel_runs(segs):
+            fn(r, out[r.channel:r.channel + r.nch])
+        torch.cuda.synchronize()
+        total += out.cpu().double()
+        for p in fn.plans.values():
+            p.close()
+    for c in range(C):
+        ref = O.fourier_llf(rgb[c].astype(np.float64), lev, K, 510.0, 20.0, 2.0)
+        assert maxerr(total[c].numpy(), ref) <= TOL_OUT
+
+
 def test_filter_host_path(F):
     img = synth.config1_image(seed=1002)
     h_in = torch.from_numpy(img).pin_memory()
