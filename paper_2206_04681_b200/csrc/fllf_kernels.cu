@@ -395,6 +395,42 @@ struct BuildWarp {
     }
   }
 
+  // Three row pairs in flight (prefetch distance 3 instead of 2): for levels
+  // >= 1, whose warps are latency-bound on their row loads (L2 round trips
+  // longer than two pairs of compute).  Pair p lives in buffer p % 3.
+  __device__ __forceinline__ void run3(int R) {
+    Pair B0, B1, B2;
+    load_pair(0, B0);
+    load_pair(1, B1);
+    load_pair(2, B2);
+    proc<false, false>(B0, 0);  // p = 0: halo rows
+    load_pair(3, B0);
+    proc<false, false>(B1, 0);  // p = 1: nothing to emit
+    if (R >= 3) load_pair(4, B1);
+    int p = 2;
+#pragma unroll 1
+    for (; p + 2 <= R; p += 3) {
+      proc<true, false>(B2, o0 + p - 2);
+      if (p + 3 <= R + 1) load_pair(p + 3, B2);
+      proc<true, false>(B0, o0 + p - 1);
+      if (p + 4 <= R + 1) load_pair(p + 4, B0);
+      proc<true, false>(B1, o0 + p);
+      if (p + 5 <= R + 1) load_pair(p + 5, B1);
+    }
+    // pairs p .. R+1 remain (1..3); the last one holds only the final row
+    const int rem = R + 2 - p;
+    if (rem == 1) {
+      proc<true, true>(B2, o0 + R - 1);
+    } else if (rem == 2) {
+      proc<true, false>(B2, o0 + p - 2);
+      proc<true, true>(B0, o0 + R - 1);
+    } else {
+      proc<true, false>(B2, o0 + p - 2);
+      proc<true, false>(B0, o0 + p - 1);
+      proc<true, true>(B1, o0 + R - 1);
+    }
+  }
+
   // Strips of exactly 2 output rows (tiny levels): every input row is loaded
   // up front, one memory round trip.
   __device__ __forceinline__ void run2() {
@@ -410,7 +446,7 @@ struct BuildWarp {
   }
 };
 
-template <int NC, int NR, bool FROM_IMAGE, bool SMALL>
+template <int NC, int NR, bool FROM_IMAGE, bool SMALL, bool DEEP = false>
 __global__ void __launch_bounds__(32) k_build(const BuildParams P) {
   pdl_wait();     // the previous level's planes are complete
   pdl_trigger();  // let the next kernel get scheduled
@@ -436,18 +472,18 @@ __global__ void __launch_bounds__(32) k_build(const BuildParams P) {
   if (interior) {
     if (zfirst) {
       BuildWarp<NC, NR, FROM_IMAGE, false, true> w(P, cb, o0, chunk, frame);
-      if (SMALL && R == 2) w.run2(); else w.template run<FROM_IMAGE>(R);
+      if (SMALL && R == 2) w.run2(); else if (DEEP && R >= 2) w.run3(R); else w.template run<FROM_IMAGE>(R);
     } else {
       BuildWarp<NC, NR, FROM_IMAGE, false, false> w(P, cb, o0, chunk, frame);
-      if (SMALL && R == 2) w.run2(); else w.template run<FROM_IMAGE>(R);
+      if (SMALL && R == 2) w.run2(); else if (DEEP && R >= 2) w.run3(R); else w.template run<FROM_IMAGE>(R);
     }
   } else {
     if (zfirst) {
       BuildWarp<NC, NR, FROM_IMAGE, true, true> w(P, cb, o0, chunk, frame);
-      if (SMALL && R == 2) w.run2(); else w.template run<FROM_IMAGE>(R);
+      if (SMALL && R == 2) w.run2(); else if (DEEP && R >= 2) w.run3(R); else w.template run<FROM_IMAGE>(R);
     } else {
       BuildWarp<NC, NR, FROM_IMAGE, true, false> w(P, cb, o0, chunk, frame);
-      if (SMALL && R == 2) w.run2(); else w.template run<FROM_IMAGE>(R);
+      if (SMALL && R == 2) w.run2(); else if (DEEP && R >= 2) w.run3(R); else w.template run<FROM_IMAGE>(R);
     }
   }
 }
@@ -1616,6 +1652,11 @@ static cudaError_t launch_build_nc(BuildParams p, int batch, cudaStream_t s, boo
   p.rows_per_strip = pick_rows(nrows, bx, batch * p.nchunks);
   dim3 grid(bx, (nrows + p.rows_per_strip - 1) / p.rows_per_strip, batch * p.nchunks);
   if (p.rows_per_strip == 2) return launch_ex(k_build<NC, 1, FROM_IMAGE, true>, grid, dim3(32), 0, s, pdl, p);
+  static const int depth = [] {  // FLLF_BUILD_DEPTH: row pairs in flight per warp (2 or 3)
+    const char* e = std::getenv("FLLF_BUILD_DEPTH");
+    return e ? std::atoi(e) : 3;  // 3 measured best on B200
+  }();
+  if (!FROM_IMAGE && depth >= 3) return launch_ex(k_build<NC, 1, FROM_IMAGE, false, true>, grid, dim3(32), 0, s, pdl, p);
   return launch_ex(k_build<NC, 1, FROM_IMAGE, false>, grid, dim3(32), 0, s, pdl, p);
 }
 
