@@ -1163,6 +1163,10 @@ __host__ __device__ constexpr int apply_cl_ctas() {
 #define FLLF_A0_UNROLL 2
 #endif
 constexpr int kApply0Unroll = FLLF_A0_UNROLL;
+#ifndef FLLF_A1_UNROLL
+#define FLLF_A1_UNROLL 1
+#endif
+constexpr int kApply1Unroll = FLLF_A1_UNROLL;  // levels >= 1 (A/B knob)
 template <bool LEVEL0, bool MAPS = false>
 __host__ __device__ constexpr int apply_cl_stages() {
   return LEVEL0 ? (FLLF_APPLY0_CTAS >= 4 ? 6 : 8) : (MAPS ? 4 : 5);
@@ -1504,7 +1508,8 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0>()) k_apply_cl(const
 
     int i = KL - 1;
     if (OPS == 2) {
-#pragma unroll kApply0Unroll
+      constexpr int UNR = MAPS ? 1 : kApply0Unroll;  // MAPS: unrolling measured slower
+#pragma unroll UNR
       for (; i >= 1; i -= 2) {
         const unsigned char* so = stage_wait();
         order(i, so, b2, b1);
@@ -1512,7 +1517,7 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0>()) k_apply_cl(const
         stage_release();
       }
     } else {
-#pragma unroll 1
+#pragma unroll kApply1Unroll
       for (; i >= 1; i -= 2) {
         order(i, stage_wait(), b2, b1);
         stage_release();
