@@ -1152,9 +1152,12 @@ __host__ __device__ constexpr int apply_cl_ops() {
 #ifndef FLLF_APPLY0_CTAS
 #define FLLF_APPLY0_CTAS 3
 #endif
-template <bool LEVEL0>
+#ifndef FLLF_MAPS1_CTAS
+#define FLLF_MAPS1_CTAS 3
+#endif
+template <bool LEVEL0, bool MAPS = false>
 __host__ __device__ constexpr int apply_cl_ctas() {
-  return LEVEL0 ? FLLF_APPLY0_CTAS : 3;
+  return LEVEL0 ? FLLF_APPLY0_CTAS : (MAPS ? FLLF_MAPS1_CTAS : 3);
 }
 // level-0 order loop unrolled over two ring stages (4 orders): the Clenshaw
 // accumulator roles then repeat without register moves (61.8 instead of
@@ -1169,7 +1172,7 @@ constexpr int kApply0Unroll = FLLF_A0_UNROLL;
 constexpr int kApply1Unroll = FLLF_A1_UNROLL;  // levels >= 1 (A/B knob)
 template <bool LEVEL0, bool MAPS = false>
 __host__ __device__ constexpr int apply_cl_stages() {
-  return LEVEL0 ? (FLLF_APPLY0_CTAS >= 4 ? 6 : 8) : (MAPS ? 4 : 5);
+  return LEVEL0 ? (FLLF_APPLY0_CTAS >= 4 ? 6 : 8) : (MAPS ? (FLLF_MAPS1_CTAS <= 2 ? 6 : 4) : 5);
 }
 template <bool LEVEL0, bool MAPS = false>
 __host__ __device__ constexpr int apply_cl_smem() {
@@ -1183,7 +1186,7 @@ __device__ __forceinline__ float ex2_approx(float x) {
 }
 
 template <bool LEVEL0, bool HAS_D, bool MAPS>
-__global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0>()) k_apply_cl(const __grid_constant__ ApplyParams P, const int ntiles) {
+__global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0, MAPS>()) k_apply_cl(const __grid_constant__ ApplyParams P, const int ntiles) {
   constexpr int S = apply_cl_stages<LEVEL0, MAPS>();
   constexpr int HB = hdr_bytes<MAPS>();
   constexpr int OPS = apply_cl_ops<LEVEL0>();
@@ -1760,7 +1763,7 @@ static cudaError_t launch_apply_t(const ApplyParams& p, int batch, cudaStream_t 
 template <bool L0, bool HD, bool MP>
 static cudaError_t launch_apply_cl_t(const ApplyParams& p, int batch, cudaStream_t s, bool pdl) {
   const int ntiles = ((p.Wf + 119) / 120) * ((p.r_end - p.r_begin + 3) / 4) * batch;
-  dim3 grid(std::min(ntiles, sm_count() * apply_cl_ctas<L0>()));
+  dim3 grid(std::min(ntiles, sm_count() * apply_cl_ctas<L0, MP>()));
   const int smem = apply_cl_smem<L0, MP>();
   static bool attr_set = false;
   if (!attr_set) {
