@@ -233,6 +233,25 @@ def test_filter_host_frames_stream(F, nb, batch):
         assert maxerr(h_out[i].numpy(), ref) <= TOL_OUT
 
 
+def test_graph_cache_buffer_pairs(F):
+    """fllf_filter keeps one CUDA graph per (input, output) buffer pair (4 cached,
+    least recently used evicted): cycling 6 distinct pairs twice re-captures
+    and replays correctly, each output equal to the first pair's result."""
+    H, W = 37, 66
+    img = synth.uniform_image(H, W, seed=77).astype(np.float32)
+    ins = [torch.from_numpy(img).cuda() for _ in range(6)]
+    outs = [torch.full((H, W), float("nan"), device="cuda") for _ in range(6)]
+    with F.Plan(H, W, 3, 5, 510.0, 30.0, 2.0) as p:
+        for _ in range(2):
+            for a, b in zip(ins, outs):
+                b.fill_(float("nan"))
+                p.filter(a, b)
+        torch.cuda.synchronize()
+    ref = O.fourier_llf(img.astype(np.float64), 3, 5, 510.0, 30.0, 2.0)
+    for b in outs:
+        assert maxerr(b.cpu().numpy(), ref) <= TOL_OUT
+
+
 def test_error_paths(F):
     with F.Plan(64, 64, 3, 4) as p:
         o = torch.empty((64, 64), device="cuda")
