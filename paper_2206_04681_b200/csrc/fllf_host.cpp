@@ -104,11 +104,12 @@ struct fllf_plan_s {
   GraphEntry graphs[kGraphCache];
   unsigned long long graph_clock = 0;
   // fllf_filter_host_frames: double-buffered device staging and the copy streams
-  float* pipe_in[2] = {nullptr, nullptr};
-  float* pipe_out[2] = {nullptr, nullptr};
+  static constexpr int kPipe = 2;  // staging slots (double-buffered; 3 measured no faster)
+  float* pipe_in[kPipe] = {};
+  float* pipe_out[kPipe] = {};
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   cudaEvent_t ev_pstart = nullptr, ev_pend = nullptr;
-  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
+  cudaEvent_t ev_in[kPipe] = {}, ev_done[kPipe] = {}, ev_out[kPipe] = {};
   void* flush_buf = nullptr;  // bench tooling: L2 flush between pipelined frames
   size_t flush_bytes = 0;
   // TMA descriptors of each level's Z planes (k_apply_cl): as the coarse
@@ -431,7 +432,7 @@ fllf_status fllf_destroy(fllf_plan p) {
     for (cudaEvent_t e : p->ev_stop) cudaEventDestroy(e);
     for (auto& g : p->graphs)
       if (g.exec) cudaGraphExecDestroy(g.exec);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < fllf_plan_s::kPipe; ++i) {
       if (p->pipe_in[i]) cudaFree(p->pipe_in[i]);
       if (p->pipe_out[i]) cudaFree(p->pipe_out[i]);
       for (cudaEvent_t ev : {p->ev_in[i], p->ev_done[i], p->ev_out[i]})
@@ -858,7 +859,7 @@ fllf_status fllf_filter_host(fllf_plan p, const float* h_img, float* h_out, void
 
 static fllf_status pipe_setup(fllf_plan p, size_t bytes) {
   if (p->pipe_in[0]) return FLLF_OK;
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < fllf_plan_s::kPipe; ++i) {
     if (cudaMalloc(&p->pipe_in[i], bytes) != cudaSuccess || cudaMalloc(&p->pipe_out[i], bytes) != cudaSuccess) {
       cudaGetLastError();
       return fail(FLLF_ERR_OUT_OF_MEMORY, "filter_host_frames: staging cudaMalloc failed");
@@ -866,10 +867,11 @@ static fllf_status pipe_setup(fllf_plan p, size_t bytes) {
   }
   cudaError_t e = cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking);
-  cudaEvent_t* evs[] = {&p->ev_pstart, &p->ev_pend, &p->ev_in[0], &p->ev_in[1], &p->ev_done[0], &p->ev_done[1],
-                        &p->ev_out[0], &p->ev_out[1]};
-  for (cudaEvent_t* ev : evs)
+  for (cudaEvent_t* ev : {&p->ev_pstart, &p->ev_pend})
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+  for (int i = 0; i < fllf_plan_s::kPipe; ++i)
+    for (cudaEvent_t* ev : {&p->ev_in[i], &p->ev_done[i], &p->ev_out[i]})
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
   return e == cudaSuccess ? FLLF_OK : cuda_fail(e, "filter_host_frames: stream / event creation");
 }
 
@@ -895,15 +897,16 @@ fllf_status fllf_filter_host_frames(fllf_plan p, const float* h_in, size_t in_st
   if (e != cudaSuccess) return cuda_fail(e, "filter_host_frames: fork");
   int launches = 0;
   for (int i = 0; i < nframes; ++i) {
-    const int b = i & 1;
-    // H2D of frame i into slot b once frame i-2's build has read it
-    if (i >= 2) e = cudaStreamWaitEvent(p->s_h2d, p->ev_done[b], 0);
+    const int b = i % fllf_plan_s::kPipe;
+    const bool reuse = i >= fllf_plan_s::kPipe;  // slot b held batch i - kPipe
+    // H2D of batch i into slot b once batch i-kPipe's build has read it
+    if (reuse) e = cudaStreamWaitEvent(p->s_h2d, p->ev_done[b], 0);
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(p->pipe_in[b], hi + (size_t)i * in_stride_bytes, bytes, cudaMemcpyHostToDevice, p->s_h2d);
     if (e == cudaSuccess) e = cudaEventRecord(p->ev_in[b], p->s_h2d);
-    // filter on s once the input has landed and frame i-2's result has left slot b
+    // filter on s once the input has landed and batch i-kPipe's result has left slot b
     if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, p->ev_in[b], 0);
-    if (e == cudaSuccess && i >= 2) e = cudaStreamWaitEvent(cs, p->ev_out[b], 0);
+    if (e == cudaSuccess && reuse) e = cudaStreamWaitEvent(cs, p->ev_out[b], 0);
     if (e == cudaSuccess && p->flush_buf) e = cudaMemsetAsync(p->flush_buf, i & 0xff, p->flush_bytes, cs);
     if (e != cudaSuccess) return cuda_fail(e, "filter_host_frames: H2D stage");
     st = fllf_filter(p, p->pipe_in[b], 0, p->pipe_out[b], 0, s);
