@@ -589,6 +589,10 @@ def main():
                 "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                 "alg_bytes_per_launch": dom[4], "avg_launch_us": round(dom[3] * 1e3, 2),
                 "share_of_step": round(dom[0] / args.steps / step_kernel_ms, 3), "peak_source": peak_src,
+                "context": ("one 1080p frame: the pyramids (47 MB) stay in the 126 MB L2 between the launches, "
+                            "so every launch is latency-bound (< 5 waves); the same kernels at config 5 "
+                            "(64 frames, HBM-bound) run at ~0.65 (level 0) and ~0.9 (level 1) of the peak: "
+                            "profiles/r01f_bench_config5.json") if args.workload == "config2" else None,
                 "timing": "per-kernel CUDA events recorded by libfllf on the launch stream over a second "
                           f"timed region of {args.steps} steps (kernels serialised: "
                           f"{prof_ms / args.steps * 1e3:.1f} us/step vs {tot_ms / args.steps * 1e3:.1f} "
