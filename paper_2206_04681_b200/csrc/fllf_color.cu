@@ -10,10 +10,10 @@
 // All three kernels are HBM-bound elementwise / small-stencil passes:
 //  k_rgb_to_yuv / k_yuv_to_rgb -- one pixel per thread, coalesced rows.
 //  k_gain_map -- 32x64 output tile per CTA; the (32+2r) x (64+2r) input
-//                window is staged in shared memory, horizontal window sums of
-//                y and y^2 are formed once per staged row, then vertical sums;
-//                sums in fp64 (E[y^2] - E[y]^2 cancels; B200 has full-rate
-//                fp64 at half the fp32 rate, and this pass is memory-bound).
+//                window is staged in shared memory; vertical window sums of y
+//                and y^2 as sliding runs per staged column, then horizontal
+//                sliding runs per output row; sums in fp64 (E[y^2] - E[y]^2
+//                cancels).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -65,51 +65,97 @@ __device__ __forceinline__ int refl_fold(int i, int n) {
 }
 
 constexpr int GT_H = 32, GT_W = 64;
+constexpr int GRUN = 8;  // outputs per sliding-window run
 
+// smem row stride (in doubles) of the vertical-sum planes: odd, so that the
+// 32 lanes of a warp reading one column of 32 different rows hit 32 banks
+__host__ __device__ constexpr int gain_vstride(int r) { return (GT_W + 2 * r) | 1; }
+
+// Window sums as sliding runs: a thread forms one full (2r+1)-tap sum and then
+// advances it by one add and one subtract per output.  The window is staged
+// once as fp64 (y - shift; warps on rows, lanes on columns: no index
+// division); vertical pass first (per staged column, two runs of 16 output
+// rows, lanes on consecutive columns), then the horizontal pass on the column
+// sums (per output row, runs of GRUN columns, lanes on consecutive rows of an
+// odd-stride plane: conflict-free); the gain values go through shared memory
+// to a coalesced store.  Interior tiles skip the reflect-101 index arithmetic.
 __global__ void __launch_bounds__(256) k_gain_map(GainParams P) {
   extern __shared__ __align__(16) unsigned char sm[];
   const int r = P.radius;
-  const int SW = GT_W + 2 * r, SH = GT_H + 2 * r;
-  float* tile = reinterpret_cast<float*>(sm);                      // SH x SW, y - shift
-  double* h1 = reinterpret_cast<double*>(sm + ((SH * SW * 4 + 15) & ~15));  // SH x GT_W
-  double* h2 = h1 + SH * GT_W;
+  const int SW = GT_W + 2 * r, SH = GT_H + 2 * r, VS = gain_vstride(r);
+  double* tile = reinterpret_cast<double*>(sm);  // SH x SW, y - shift
+  double* v1 = tile + SH * SW;                   // GT_H x VS
+  double* v2 = v1 + GT_H * VS;
+  float* gout = reinterpret_cast<float*>(tile);  // GT_H x (GT_W + 1), reuses the window after the vertical pass
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int y0 = blockIdx.y * GT_H, x0 = blockIdx.x * GT_W;
   // shift by one sample of the tile: variance is shift-invariant, the sums stay small
   const float shift = __ldg(P.y + (long long)min(y0, P.H - 1) * P.y_pitch + min(x0, P.W - 1));
-  for (int t = threadIdx.x; t < SH * SW; t += blockDim.x) {
-    const int ty = t / SW, tx = t - ty * SW;
-    const int gy = refl_fold(y0 - r + ty, P.H), gx = refl_fold(x0 - r + tx, P.W);
-    tile[t] = __ldg(P.y + (long long)gy * P.y_pitch + gx) - shift;
+  const bool interior = y0 - r >= 0 && y0 + GT_H + r <= P.H && x0 - r >= 0 && x0 + GT_W + r <= P.W;
+  if (interior) {
+    for (int ty = warp; ty < SH; ty += 8) {
+      const float* src = P.y + (long long)(y0 - r + ty) * P.y_pitch + (x0 - r);
+      for (int tx = lane; tx < SW; tx += 32) tile[ty * SW + tx] = (double)(__ldg(src + tx) - shift);
+    }
+  } else {
+    for (int ty = warp; ty < SH; ty += 8) {
+      const float* src = P.y + (long long)refl_fold(y0 - r + ty, P.H) * P.y_pitch;
+      for (int tx = lane; tx < SW; tx += 32)
+        tile[ty * SW + tx] = (double)(__ldg(src + refl_fold(x0 - r + tx, P.W)) - shift);
+    }
   }
   __syncthreads();
-  // horizontal window sums for every staged row, the GT_W output columns
-  for (int t = threadIdx.x; t < SH * GT_W; t += blockDim.x) {
-    const int ty = t / GT_W, tx = t - ty * GT_W;
-    const float* row = tile + ty * SW + tx;
+  // vertical: per staged column, two runs of GT_H / 2 output rows
+  constexpr int VR = GT_H / 2;
+  for (int t = threadIdx.x; t < 2 * SW; t += blockDim.x) {
+    const int col = t < SW ? t : t - SW, r0 = t < SW ? 0 : VR;
+    const double* c = tile + r0 * SW + col;
     double s1 = 0.0, s2 = 0.0;
     for (int d = 0; d <= 2 * r; ++d) {
-      const double v = row[d];
+      const double v = c[d * SW];
       s1 += v;
       s2 = fma(v, v, s2);
     }
-    h1[t] = s1;
-    h2[t] = s2;
+    v1[r0 * VS + col] = s1;
+    v2[r0 * VS + col] = s2;
+#pragma unroll 4
+    for (int q = 1; q < VR; ++q) {
+      const double vin = c[(q + 2 * r) * SW], vout = c[(q - 1) * SW];
+      s1 += vin - vout;
+      s2 += fma(vin, vin, -vout * vout);
+      v1[(r0 + q) * VS + col] = s1;
+      v2[(r0 + q) * VS + col] = s2;
+    }
   }
   __syncthreads();
+  // horizontal: per output row, runs of GRUN output columns (lanes = rows)
   const double inv_n = 1.0 / ((2.0 * r + 1.0) * (2.0 * r + 1.0));
-  for (int t = threadIdx.x; t < GT_H * GT_W; t += blockDim.x) {
-    const int ty = t / GT_W, tx = t - ty * GT_W;
-    const int gy = y0 + ty, gx = x0 + tx;
-    if (gy >= P.H || gx >= P.W) continue;
+  {
+    const int row = threadIdx.x % GT_H, c0 = (threadIdx.x / GT_H) * GRUN;  // 256 = GT_H x GT_W / GRUN
+    const double* a1 = v1 + row * VS + c0;
+    const double* a2 = v2 + row * VS + c0;
     double s1 = 0.0, s2 = 0.0;
     for (int d = 0; d <= 2 * r; ++d) {
-      s1 += h1[(ty + d) * GT_W + tx];
-      s2 += h2[(ty + d) * GT_W + tx];
+      s1 += a1[d];
+      s2 += a2[d];
     }
-    const double mean = s1 * inv_n;
-    const double var = fmax(s2 * inv_n - mean * mean, 0.0);
-    const double g = P.m_lo + (P.m_hi - P.m_lo) * fmin(1.0, var * P.inv_vref);
-    P.m[(long long)gy * P.m_pitch + gx] = (float)g;
+#pragma unroll
+    for (int q = 0; q < GRUN; ++q) {
+      if (q > 0) {
+        s1 += a1[q + 2 * r] - a1[q - 1];
+        s2 += a2[q + 2 * r] - a2[q - 1];
+      }
+      const double mean = s1 * inv_n;
+      const double var = fmax(s2 * inv_n - mean * mean, 0.0);
+      gout[row * (GT_W + 1) + c0 + q] = (float)(P.m_lo + (P.m_hi - P.m_lo) * fmin(1.0, var * P.inv_vref));
+    }
+  }
+  __syncthreads();
+  for (int ty = warp; ty < GT_H; ty += 8) {
+    const int gy = y0 + ty;
+    if (gy >= P.H) break;
+    for (int tx = lane; tx < GT_W; tx += 32)
+      if (x0 + tx < P.W) P.m[(long long)gy * P.m_pitch + x0 + tx] = gout[ty * (GT_W + 1) + tx];
   }
 }
 
@@ -140,7 +186,7 @@ cudaError_t launch_yuv_to_rgb(const ColorParams& p, cudaStream_t s) {
 
 size_t gain_map_smem(int radius) {
   const int SW = GT_W + 2 * radius, SH = GT_H + 2 * radius;
-  return (size_t)((SH * SW * 4 + 15) & ~15) + 2 * sizeof(double) * SH * GT_W;
+  return sizeof(double) * ((size_t)SH * SW + 2 * (size_t)GT_H * gain_vstride(radius));
 }
 
 cudaError_t launch_gain_map(const GainParams& p, cudaStream_t s) {
