@@ -93,9 +93,14 @@ __global__ void __launch_bounds__(256) k_gain_map(GainParams P) {
   const float shift = __ldg(P.y + (long long)min(y0, P.H - 1) * P.y_pitch + min(x0, P.W - 1));
   const bool interior = y0 - r >= 0 && y0 + GT_H + r <= P.H && x0 - r >= 0 && x0 + GT_W + r <= P.W;
   if (interior) {
-    for (int ty = warp; ty < SH; ty += 8) {
-      const float* src = P.y + (long long)(y0 - r + ty) * P.y_pitch + (x0 - r);
-      for (int tx = lane; tx < SW; tx += 32) tile[ty * SW + tx] = (double)(__ldg(src + tx) - shift);
+    // SW <= 128: at most four 32-column passes per row, unrolled
+    const float* src = P.y + (long long)(y0 - r + warp) * P.y_pitch + (x0 - r) + lane;
+    const long long step = 8 * P.y_pitch;
+    double* dst = tile + warp * SW + lane;
+    for (int ty = warp; ty < SH; ty += 8, src += step, dst += 8 * SW) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (lane + 32 * u < SW) dst[32 * u] = (double)(__ldg(src + 32 * u) - shift);
     }
   } else {
     for (int ty = warp; ty < SH; ty += 8) {
@@ -130,6 +135,7 @@ __global__ void __launch_bounds__(256) k_gain_map(GainParams P) {
   __syncthreads();
   // horizontal: per output row, runs of GRUN output columns (lanes = rows)
   const double inv_n = 1.0 / ((2.0 * r + 1.0) * (2.0 * r + 1.0));
+  const float mlo = (float)P.m_lo, dm = (float)(P.m_hi - P.m_lo), ivr = (float)P.inv_vref;
   {
     const int row = threadIdx.x % GT_H, c0 = (threadIdx.x / GT_H) * GRUN;  // 256 = GT_H x GT_W / GRUN
     const double* a1 = v1 + row * VS + c0;
@@ -146,8 +152,8 @@ __global__ void __launch_bounds__(256) k_gain_map(GainParams P) {
         s2 += a2[q + 2 * r] - a2[q - 1];
       }
       const double mean = s1 * inv_n;
-      const double var = fmax(s2 * inv_n - mean * mean, 0.0);
-      gout[row * (GT_W + 1) + c0 + q] = (float)(P.m_lo + (P.m_hi - P.m_lo) * fmin(1.0, var * P.inv_vref));
+      const float var = (float)fma(s2, inv_n, -mean * mean);  // fp64 where it cancels, fp32 after
+      gout[row * (GT_W + 1) + c0 + q] = fmaf(dm, fminf(1.f, fmaxf(var, 0.f) * ivr), mlo);
     }
   }
   __syncthreads();
