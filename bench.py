@@ -147,7 +147,7 @@ def algorithmic_bytes(kind, level, dims, K, frames, levels):
 
 
 # ------------------------------------------------------------ CPU baseline
-def cpu_baseline(img, c, budget_s=12.0, max_frames=3):
+def cpu_baseline(img, c, budget_s=12.0, max_frames=6):
     """The oracle as it stands (numpy fp64), on full frames of the workload."""
     from oracle import fllf_oracle as O
     n, t0 = 0, time.perf_counter()
