@@ -200,8 +200,10 @@ struct BuildWarp {
     // halo columns of the destination Z planes (see ZHALO): col -1 := x_1,
     // col Wc := x_{Wc-1} (Wf even) or x_{Wc-2} (Wf odd)
     // (both can hold for one lane when Wc = 3)
-    halo_l = store_lane && x == 1;
-    halo_r = store_lane && x == ((P.Wf & 1) ? P.Wc - 2 : P.Wc - 1);
+    // (only edge warps can hold them: interior warps start at fine column >= 58
+    // and end before the last fine column, so the stores compile out there)
+    halo_l = EDGE && store_lane && x == 1;
+    halo_r = EDGE && store_lane && x == ((P.Wf & 1) ? P.Wc - 2 : P.Wc - 1);
     hoff_r = P.Wc - x;
     if (FROM_IMAGE) {
       rsrc[0] = P.img.p + frame * P.img.fstride;
