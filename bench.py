@@ -585,7 +585,9 @@ def main():
         try:
             tj = json.load(open(tp))
             key = f"{args.workload}:{dom[1]}:{dom[2]}"
-            traffic = tj.get(key)
+            traffic = tj.get(key)  # per frame of the capture's batch
+            if traffic is not None:
+                traffic = int(traffic * frames)
         except Exception:
             traffic = None
     roofline = {"bound": "hbm", "kernel": f"{dom[1]} (level {dom[2]})", "achieved": round(achieved, 1),

@@ -1,11 +1,12 @@
 """Summarise an ncu report (--set full) into markdown + roofline traffic json.
 
-    python tools/ncu_summary.py gpurun_out/prof.ncu-rep profiles/r01_ncu_full.md [workload [levels]]
+    python tools/ncu_summary.py gpurun_out/prof.ncu-rep profiles/r01_ncu_full.md [workload [levels [frames]]]
 
 With `levels`, the launches are taken as one filter sequence (build0,
 build 1..levels-2, apply levels-2..1, apply0) and their DRAM read+write bytes
-are merged into profiles/roofline_traffic.json under "<workload>:<kind>:<level>"
-(read by bench.py for the roofline `traffic` field).
+PER FRAME (the capture's bytes / `frames`, the batch the capture ran) are
+merged into profiles/roofline_traffic.json under "<workload>:<kind>:<level>";
+bench.py multiplies by its own batch for the roofline `traffic` field.
 """
 import csv
 import io
@@ -79,8 +80,9 @@ if len(sys.argv) > 4:
         tp = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
                           "roofline_traffic.json")
         tj = json.load(open(tp)) if os.path.exists(tp) else {}
+        frames = int(sys.argv[5]) if len(sys.argv) > 5 else 1
         for (kind, lev), b in zip(order, rows_bytes[:len(order)]):
-            tj[f"{workload}:{kind}:{lev}"] = round(b)
+            tj[f"{workload}:{kind}:{lev}"] = round(b / frames)
         json.dump(tj, open(tp, "w"), indent=1, sort_keys=True)
         print("traffic ->", tp)
 
