@@ -69,6 +69,9 @@ struct fllf_plan_s {
   void* ws = nullptr;
   size_t ws_bytes = 0;
   void* maps_ws = nullptr;
+  size_t maps_ws_bytes = 0;
+  const char* dbg_out_lo = nullptr;  // debug-bounds builds: the current apply's output range
+  const char* dbg_out_hi = nullptr;
   bool built = false;
   const float* img = nullptr;  // the image of the most recent build
   long long img_pitch = 0;     // floats
@@ -485,6 +488,8 @@ static fllf_status build_level_impl(fllf_plan p, const float* img, long long pit
   bp.o_end = p->be[l + 1];
   bp.fr_lo = p->al[l];
   bp.fr_hi = p->ah[l];
+  bp.dbg_lo = static_cast<const char*>(p->ws);
+  bp.dbg_hi = bp.dbg_lo + p->ws_bytes;
   cudaError_t e;
   {
     ProfScope ps(p, stream, l == 0 ? FLLF_K_BUILD0 : FLLF_K_BUILD, l);
@@ -548,6 +553,7 @@ static fllf_status ensure_maps_ws(fllf_plan p) {
     cudaGetLastError();
     return fail(FLLF_ERR_OUT_OF_MEMORY, "map pyramid cudaMalloc failed");
   }
+  p->maps_ws_bytes = off;
   char* base = static_cast<char*>(p->maps_ws);
   for (int l = 1; l < p->nlev; ++l) {
     p->lv[l].MS = reinterpret_cast<float*>(base + offs[l]);
@@ -597,6 +603,18 @@ static fllf_status apply_level_impl(fllf_plan p, fllf::ApplyParams& ap, int l, b
   ap.fr_hi = p->ah[l];
   const bool has_d = (l + 1) < lmax;  // D_lmax = 0
   ap.wait_first = (l == lmax - 1 || !pdl) ? 1 : 0;
+  if (l == 0) {
+    ap.dbg_lo = p->dbg_out_lo;
+    ap.dbg_hi = p->dbg_out_hi;
+  } else {
+    ap.dbg_lo = static_cast<const char*>(p->ws);
+    ap.dbg_hi = ap.dbg_lo + p->ws_bytes;
+  }
+  static const bool dbg_selftest = [] {  // debug-bounds builds: an empty range must trap
+    const char* e = std::getenv("FLLF_DEBUG_BOUNDS_SELFTEST");
+    return e && e[0] == '1';
+  }();
+  if (dbg_selftest) ap.dbg_hi = ap.dbg_lo;
   cudaError_t e;
   {
     ProfScope ps(p, stream, l == 0 ? FLLF_K_APPLY0 : FLLF_K_APPLY, l);
@@ -632,6 +650,10 @@ static fllf_status apply_impl(fllf_plan p, const fllf_apply_args* a, float* d_ou
   ap.img.pitch = p->img_pitch;
   ap.img.fstride = p->img_pitch * p->d.H;
   ap.out = d_out - (long long)p->d.row_begin * opitch;  // global row 0 (bands: virtual)
+  // debug-bounds builds: level 0 writes the caller's rows, levels >= 1 the workspace
+  p->dbg_out_lo = reinterpret_cast<const char*>(d_out);
+  p->dbg_out_hi = p->dbg_out_lo + ((size_t)(p->d.batch - 1) * p->d.H + (p->d.row_end - p->d.row_begin)) *
+                                      (size_t)opitch * sizeof(float);
   ap.out_pitch = opitch;
   ap.out_fstride = opitch * p->d.H;
   ap.KL = p->KL;
@@ -705,6 +727,8 @@ static fllf_status apply_impl(fllf_plan p, const fllf_apply_args* a, float* d_ou
       bp.fr_lo = 0;
       bp.fr_hi = p->Hs[l] - 1;
       bp.invT = (float)(1.0 / T);
+      bp.dbg_lo = static_cast<const char*>(p->maps_ws);  // the map pyramids
+      bp.dbg_hi = bp.dbg_lo + p->maps_ws_bytes;
       cudaError_t e;
       {
         ProfScope ps(p, stream, FLLF_K_MAPBUILD, l);

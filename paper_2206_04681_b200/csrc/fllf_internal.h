@@ -63,6 +63,8 @@ struct BuildParams {
   // changes rows that feed no stored output.
   int o_begin, o_end;
   int fr_lo, fr_hi;
+  const char* dbg_lo;  // FLLF_DEBUG_BOUNDS builds: every global store must land in [dbg_lo, dbg_hi)
+  const char* dbg_hi;
 };
 
 struct ApplyParams {
@@ -108,6 +110,8 @@ struct ApplyParams {
   // used only for boxes inside those ranges.
   int r_begin, r_end;
   int cr_lo, cr_hi, fr_lo, fr_hi;
+  const char* dbg_lo;  // FLLF_DEBUG_BOUNDS builds: every global store must land in [dbg_lo, dbg_hi)
+  const char* dbg_hi;
 };
 
 // Colour conversion (fllf_color.cu): three planes in, three planes out, all

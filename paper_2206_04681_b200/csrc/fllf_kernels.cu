@@ -36,6 +36,7 @@
 //              warp shuffles.
 //
 // No tensor cores: this is a stencil + elementwise path (no contraction).
+#include <cstdio>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <cstdlib>
@@ -48,6 +49,24 @@ namespace fllf {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
+
+// Debug-bounds builds (`build --variant dbg -DFLLF_DEBUG_BOUNDS`; compute-
+// sanitizer is closed on this GPU pool): every global store of the pyramid
+// kernels is checked against the range the host declared for the launch
+// (the plan workspace, or the caller's output) and traps on a miss.
+#ifdef FLLF_DEBUG_BOUNDS
+#define FLLF_DBG_STORE(P, ptr, nbytes)                                                                       \
+  do {                                                                                                      \
+    const char* p_ = reinterpret_cast<const char*>(ptr);                                                   \
+    if (p_ < (P).dbg_lo || p_ + (nbytes) > (P).dbg_hi) {                                                    \
+      printf("fllf bounds: line %d block (%d,%d,%d) thread %d\n", __LINE__, blockIdx.x, blockIdx.y,        \
+             blockIdx.z, threadIdx.x);                                                                      \
+      __trap();                                                                                             \
+    }                                                                                                       \
+  } while (0)
+#else
+#define FLLF_DBG_STORE(P, ptr, nbytes) ((void)0)
+#endif
 // [1,4,6,4,1]/16
 constexpr float W0 = 0.375f, W1 = 0.25f, W2 = 0.0625f;
 constexpr float TWO_PI = 6.28318530717958647692f;
@@ -274,9 +293,18 @@ struct BuildWarp {
       const float2 ea = pfma(bc(W2), ea_, Pv[0]);
       const float2 eb = pfma(bc(W2), eb_, Pv[1]);
       const float2 h = hfilt_c(ea, eb);
-      if (store_lane) q[0] = h;
-      if (halo_l) q[-2] = h;  // x == 1: column -1
-      if (halo_r) q[hoff_r] = h;
+      if (store_lane) {
+        FLLF_DBG_STORE(P, q, 8);
+        q[0] = h;
+      }
+      if (halo_l) {
+        FLLF_DBG_STORE(P, q - 2, 8);
+        q[-2] = h;  // x == 1: column -1
+      }
+      if (halo_r) {
+        FLLF_DBG_STORE(P, q + hoff_r, 8);
+        q[hoff_r] = h;
+      }
     }
     if (!ONLY) {
       vstep_fixed(Pv[0], Av[0], ea_, oa);
@@ -294,7 +322,10 @@ struct BuildWarp {
         if (EMIT) {
           const float2 e = pfma(bc(W2), d.e.r[i], Pr[i]);
           const float h = hfilt_r(e.x, e.y);
-          if (store_lane) rdst[i][(long long)emit * P.dst.pitch + x] = h;
+          if (store_lane) {
+            FLLF_DBG_STORE(P, rdst[i] + (long long)emit * P.dst.pitch + x, 4);
+            rdst[i][(long long)emit * P.dst.pitch + x] = h;
+          }
         }
         if (!ONLY) vstep_fixed(Pr[i], Ar[i], d.e.r[i], d.o.r[i]);
       }
@@ -604,7 +635,10 @@ struct Build0Warp {
         const float La = __shfl_up_sync(FULL, a, 1), Lb = __shfl_up_sync(FULL, b, 1);
         const float Ra = __shfl_down_sync(FULL, a, 1);
         const float h = fmaf(6.f, a, fmaf(4.f, b + Lb, La + Ra)) * (1.f / 256.f);
-        if (store_lane) gdst[emit * P.dst.pitch + x] = h;
+        if (store_lane) {
+          FLLF_DBG_STORE(P, gdst + emit * P.dst.pitch + x, 4);
+          gdst[emit * P.dst.pitch + x] = h;
+        }
       }
       if (!ONLY) {
         Pr = pfma(bc(6.f), d.e, pfma(bc(4.f), d.o, Ar));
@@ -641,10 +675,19 @@ struct Build0Warp {
         const float2 eb = padd(Pc[i][1], zc[1]);
         const float2 h = hsum_c(ea, eb);
         float2* q = wide_off(zdst, (unsigned)(off0 + i * (int)P.dst.kstride_z));
-        if (store_lane) stg2(q, h);
+        if (store_lane) {
+          FLLF_DBG_STORE(P, q, 8);
+          stg2(q, h);
+        }
         if (EDGE) {
-          if (halo_l) q[-2] = h;  // x == 1: column -1
-          if (halo_r) q[P.Wc - x] = h;
+          if (halo_l) {
+            FLLF_DBG_STORE(P, q - 2, 8);
+            q[-2] = h;  // x == 1: column -1
+          }
+          if (halo_r) {
+            FLLF_DBG_STORE(P, q + (P.Wc - x), 8);
+            q[P.Wc - x] = h;
+          }
         }
       }
       if (!ONLY) {
@@ -1092,12 +1135,16 @@ __global__ void __launch_bounds__(160, MAPS ? 2 : 3) k_apply(const ApplyParams P
         if (2 * r + tt >= P.Hf) break;
         float* rp = op + (long long)(2 * r + tt) * opitch;
         if (fvec_ok && oal) {
+          FLLF_DBG_STORE(P, rp + xf0, 16);
           *reinterpret_cast<float4*>(rp + xf0) =
               make_float4(res[4 * tt], res[4 * tt + 1], res[4 * tt + 2], res[4 * tt + 3]);
         } else {
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            if (xf0 + q < P.Wf) rp[xf0 + q] = res[4 * tt + q];
+            if (xf0 + q < P.Wf) {
+              FLLF_DBG_STORE(P, rp + xf0 + q, 4);
+              rp[xf0 + q] = res[4 * tt + q];
+            }
         }
       }
     }
@@ -1616,12 +1663,16 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0, MAPS>()) k_apply_cl
         if (2 * r + tt >= P.Hf) break;
         float* rp = op + (long long)(2 * r + tt) * opitch;
         if (fvec_ok && oal) {
+          FLLF_DBG_STORE(P, rp + xf0, 16);
           *reinterpret_cast<float4*>(rp + xf0) =
               make_float4(res[4 * tt], res[4 * tt + 1], res[4 * tt + 2], res[4 * tt + 3]);
         } else {
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            if (xf0 + q < P.Wf) rp[xf0 + q] = res[4 * tt + q];
+            if (xf0 + q < P.Wf) {
+              FLLF_DBG_STORE(P, rp + xf0 + q, 4);
+              rp[xf0 + q] = res[4 * tt + q];
+            }
         }
       }
     }
