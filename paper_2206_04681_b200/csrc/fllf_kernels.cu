@@ -257,10 +257,13 @@ struct BuildWarp {
 
   __device__ __forceinline__ void load_row(int row, Row& d) const {
     const int rr = min(max(refl101(row, P.Hf), P.fr_lo), P.fr_hi);
+    // real rows only for the warps that filter them (chunk 0; every map-build warp)
+    if (do_real || FROM_IMAGE || NC == 0) {
 #pragma unroll
-    for (int i = 0; i < NR; ++i) {
-      const float* rp = rsrc[i] + (long long)rr * rpitch;
-      d.r[i] = EDGE ? make_float2(__ldg(rp + rc0), __ldg(rp + rc1)) : ldg2(rp + c0);
+      for (int i = 0; i < NR; ++i) {
+        const float* rp = rsrc[i] + (long long)rr * rpitch;
+        d.r[i] = EDGE ? make_float2(__ldg(rp + rc0), __ldg(rp + rc1)) : ldg2(rp + c0);
+      }
     }
     if (!FROM_IMAGE && NC > 0) {
       const float2* q = zsrc + (long long)rr * P.src.zpitch;
