@@ -412,13 +412,30 @@ def run_sharded(args, c, wl, world, rank, local):
     rgb = synth.config3_rgb()
     img = torch.from_numpy(rgb).cuda()
     out = torch.empty_like(img)
-    fn = D.gpu_partial_fn(img, levels, K, c["T"], c["sigma_r"], c["m"])
+    if args.combine == "p2p":
+        comb = D.P2PCombine(img, levels, K, c["T"], c["sigma_r"], c["m"])
+        fn = None
+
+        def step():
+            comb.run()
+
+        def step_launches():
+            return sum(p.launches for _, p in comb.jobs)
+    else:
+        comb = None
+        fn = D.gpu_partial_fn(img, levels, K, c["T"], c["sigma_r"], c["m"])
+
+        def step():
+            D.sharded_filter(fn, out, 3, K, batch_channels=True)
+
+        def step_launches():
+            return sum(p.launches for p in fn.plans.values())
     l2 = torch.cuda.get_device_properties(local).L2_cache_size or 126 * 2 ** 20
     flush_buf = torch.empty(2 * l2 // 4 + 1024, dtype=torch.float32, device="cuda")
     stream = torch.cuda.current_stream()
     for _ in range(max(args.warmup, 1)):
         flush_buf.zero_()
-        D.sharded_filter(fn, out, 3, K, batch_channels=True)
+        step()
     torch.cuda.synchronize()
     dist.barrier()
     clk = ClockSampler(local)
@@ -429,9 +446,9 @@ def run_sharded(args, c, wl, world, rank, local):
     for i in range(args.steps):
         flush_buf.zero_()
         starts[i].record(stream)
-        D.sharded_filter(fn, out, 3, K, batch_channels=True)
+        step()
         ends[i].record(stream)
-        launches += sum(p.launches for p in fn.plans.values())
+        launches += step_launches()
     torch.cuda.synchronize()
     clk.stop()
     dist.barrier()
@@ -446,12 +463,17 @@ def run_sharded(args, c, wl, world, rank, local):
                 "data": "synthetic",
                 "config": {"workload": wl["desc"], "H": H, "W": W, "channels": 3, "levels": levels, "K": K,
                            "parallelism": f"order-shard{world}",
+                           "combine": ("fused: fllf_apply_accumulate into the owner's IPC-mapped output"
+                                       if comb is not None else "NCCL reduce per channel"),
                            "l2": f"flushed between timed steps ({flush_buf.numel() * 4 >> 20} MiB write)"},
                 "gpu_launches": launches, "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     clk.close()
-    for p in fn.plans.values():
-        p.close()
+    if comb is not None:
+        comb.close()
+    else:
+        for p in fn.plans.values():
+            p.close()
     dist.destroy_process_group()
     return 0
 
@@ -466,6 +488,9 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="config2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--combine", choices=["nccl", "p2p"], default="nccl",
+                    help="config3: NCCL reduce per channel, or the fused combine "
+                         "(fllf_apply_accumulate into the owner's CUDA-IPC-mapped output)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

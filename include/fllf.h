@@ -141,6 +141,31 @@ FLLF_API fllf_status fllf_build_fourier_pyramids(fllf_plan p, const float* d_img
 FLLF_API fllf_status fllf_apply(fllf_plan p, const fllf_apply_args* a, float* d_out,
                        size_t out_pitch_bytes, void* s);
 
+/* As fllf_apply (SCALAR / COEFFS, full-frame plans), but the level-0 result is
+ * ADDED to d_out with hardware atomics instead of stored: the combine step of
+ * order sharding (linearity of Eq. 4) fused into the apply's
+ * epilogue.  d_out may be another GPU's buffer mapped through CUDA IPC
+ * (fllf_ipc_open): every rank adds its partial output straight into the
+ * owner's frame over NVLink, no separate reduce.  The caller zeroes d_out once
+ * before the first partial and orders all partials before reading it; the
+ * summation order is not fixed (fp32 atomics: results agree to rounding).
+ * MAPS or row-band plans: FLLF_ERR_INVALID_ARGUMENT. */
+FLLF_API fllf_status fllf_apply_accumulate(fllf_plan p, const fllf_apply_args* a, float* d_out,
+                                           size_t out_pitch_bytes, void* s);
+
+/* CUDA IPC plumbing for fllf_apply_accumulate across processes (host logic,
+ * no kernels): fllf_ipc_alloc allocates `bytes` of device memory on the
+ * current device and writes its FLLF_IPC_HANDLE_BYTES-byte IPC handle to
+ * handle_out; fllf_ipc_open maps a handle from another process into this one
+ * (peer access enabled lazily); fllf_ipc_close / fllf_ipc_free undo them.
+ * Errors: FLLF_ERR_BAD_POINTER (NULL / 0 bytes), FLLF_ERR_OUT_OF_MEMORY,
+ * FLLF_ERR_CUDA (the runtime refused, e.g. a handle from this same process). */
+#define FLLF_IPC_HANDLE_BYTES 64
+FLLF_API fllf_status fllf_ipc_alloc(size_t bytes, void** d_ptr, void* handle_out);
+FLLF_API fllf_status fllf_ipc_free(void* d_ptr);
+FLLF_API fllf_status fllf_ipc_open(const void* handle, void** d_ptr);
+FLLF_API fllf_status fllf_ipc_close(void* d_ptr);
+
 /* build + apply(SCALAR) in one call (the common one-shot filter).  The launch
  * sequence is captured once into a CUDA graph (per plan, input/output buffer
  * pair and profiling flag) and replayed on `s`; FLLF_NO_GRAPH=1 in the

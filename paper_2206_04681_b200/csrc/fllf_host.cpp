@@ -626,7 +626,7 @@ static fllf_status apply_level_impl(fllf_plan p, fllf::ApplyParams& ap, int l, b
 // fllf_apply (only_level < 0: the whole coarse-to-fine pass) and
 // fllf_apply_level (only that level).
 static fllf_status apply_impl(fllf_plan p, const fllf_apply_args* a, float* d_out, size_t out_pitch_bytes, void* s,
-                              int only_level) {
+                              int only_level, bool accumulate = false) {
   if (!p) return fail(FLLF_ERR_BAD_POINTER, "NULL plan");
   if (!p->built) return fail(FLLF_ERR_NOT_BUILT, "fllf_apply before fllf_build_fourier_pyramids");
   long long opitch;
@@ -650,6 +650,7 @@ static fllf_status apply_impl(fllf_plan p, const fllf_apply_args* a, float* d_ou
   ap.img.pitch = p->img_pitch;
   ap.img.fstride = p->img_pitch * p->d.H;
   ap.out = d_out - (long long)p->d.row_begin * opitch;  // global row 0 (bands: virtual)
+  ap.accumulate = accumulate ? 1 : 0;
   // debug-bounds builds: level 0 writes the caller's rows, levels >= 1 the workspace
   p->dbg_out_lo = reinterpret_cast<const char*>(d_out);
   p->dbg_out_hi = p->dbg_out_lo + ((size_t)(p->d.batch - 1) * p->d.H + (p->d.row_end - p->d.row_begin)) *
@@ -751,6 +752,54 @@ static fllf_status apply_impl(fllf_plan p, const fllf_apply_args* a, float* d_ou
 
 fllf_status fllf_apply(fllf_plan p, const fllf_apply_args* a, float* d_out, size_t out_pitch_bytes, void* s) {
   return apply_impl(p, a, d_out, out_pitch_bytes, s, -1);
+}
+
+fllf_status fllf_apply_accumulate(fllf_plan p, const fllf_apply_args* a, float* d_out, size_t out_pitch_bytes,
+                                  void* s) {
+  if (!p) return fail(FLLF_ERR_BAD_POINTER, "NULL plan");
+  if (a && a->mode == FLLF_MAPS) return fail(FLLF_ERR_INVALID_ARGUMENT, "apply_accumulate: SCALAR / COEFFS only");
+  if (p->band) return fail(FLLF_ERR_INVALID_ARGUMENT, "apply_accumulate: not for row-band plans");
+  return apply_impl(p, a, d_out, out_pitch_bytes, s, -1, true);
+}
+
+fllf_status fllf_ipc_alloc(size_t bytes, void** d_ptr, void* handle_out) {
+  if (!d_ptr || !handle_out || bytes == 0) return fail(FLLF_ERR_BAD_POINTER, "ipc_alloc: NULL argument or 0 bytes");
+  *d_ptr = nullptr;
+  cudaError_t e = cudaMalloc(d_ptr, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(FLLF_ERR_OUT_OF_MEMORY, "ipc_alloc: cudaMalloc failed");
+  }
+  cudaIpcMemHandle_t h;
+  e = cudaIpcGetMemHandle(&h, *d_ptr);
+  if (e != cudaSuccess) {
+    cudaFree(*d_ptr);
+    *d_ptr = nullptr;
+    return cuda_fail(e, "cudaIpcGetMemHandle");
+  }
+  std::memcpy(handle_out, &h, sizeof(h));
+  return FLLF_OK;
+}
+
+fllf_status fllf_ipc_free(void* d_ptr) {
+  if (!d_ptr) return FLLF_OK;
+  cudaError_t e = cudaFree(d_ptr);
+  return e == cudaSuccess ? FLLF_OK : cuda_fail(e, "ipc_free: cudaFree");
+}
+
+fllf_status fllf_ipc_open(const void* handle, void** d_ptr) {
+  if (!handle || !d_ptr) return fail(FLLF_ERR_BAD_POINTER, "ipc_open: NULL argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  *d_ptr = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  return e == cudaSuccess ? FLLF_OK : cuda_fail(e, "cudaIpcOpenMemHandle");
+}
+
+fllf_status fllf_ipc_close(void* d_ptr) {
+  if (!d_ptr) return FLLF_OK;
+  cudaError_t e = cudaIpcCloseMemHandle(d_ptr);
+  return e == cudaSuccess ? FLLF_OK : cuda_fail(e, "cudaIpcCloseMemHandle");
 }
 
 fllf_status fllf_apply_level(fllf_plan p, const fllf_apply_args* a, float* d_out, size_t out_pitch_bytes, int level,

@@ -110,6 +110,7 @@ struct ApplyParams {
   // used only for boxes inside those ranges.
   int r_begin, r_end;
   int cr_lo, cr_hi, fr_lo, fr_hi;
+  int accumulate;      // level 0: atomically add the output into out (fllf_apply_accumulate)
   const char* dbg_lo;  // FLLF_DEBUG_BOUNDS builds: every global store must land in [dbg_lo, dbg_hi)
   const char* dbg_hi;
 };

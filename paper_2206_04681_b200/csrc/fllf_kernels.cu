@@ -1665,7 +1665,23 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0, MAPS>()) k_apply_cl
       for (int tt = 0; tt < 2; ++tt) {
         if (2 * r + tt >= P.Hf) break;
         float* rp = op + (long long)(2 * r + tt) * opitch;
-        if (fvec_ok && oal) {
+        if (LEVEL0 && P.accumulate) {
+          // fused combine (order sharding): add this partial output into the
+          // destination -- local, or a peer GPU's buffer mapped through CUDA
+          // IPC, the adds then travel over NVLink -- with hardware atomics
+          if (fvec_ok && oal) {
+            FLLF_DBG_STORE(P, rp + xf0, 16);
+            atomicAdd(reinterpret_cast<float4*>(rp + xf0),
+                      make_float4(res[4 * tt], res[4 * tt + 1], res[4 * tt + 2], res[4 * tt + 3]));
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (xf0 + q < P.Wf) {
+                FLLF_DBG_STORE(P, rp + xf0 + q, 4);
+                atomicAdd(rp + xf0 + q, res[4 * tt + q]);
+              }
+          }
+        } else if (fvec_ok && oal) {
           FLLF_DBG_STORE(P, rp + xf0, 16);
           *reinterpret_cast<float4*>(rp + xf0) =
               make_float4(res[4 * tt], res[4 * tt + 1], res[4 * tt + 2], res[4 * tt + 3]);

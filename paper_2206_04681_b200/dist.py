@@ -154,6 +154,74 @@ def gpu_partial_fn(img, levels: int, K: int, T: float, sigma_r: float, m: float)
     return fn
 
 
+class P2PCombine:
+    """Order sharding with the combine fused into the level-0 apply (a7): the
+    owner rank allocates the (channels, H, W) output with fllf_ipc_alloc and
+    shares its CUDA IPC handle; every rank maps it and its partial plans add
+    their outputs straight into it with fllf_apply_accumulate (hardware atomics;
+    over NVLink when the owner is another GPU) -- no partial buffers, no
+    separate reduce.  Per call: owner zeroes, barrier, partials, barrier.
+
+    img: (channels, H, W) CUDA tensor on this rank's device (every rank holds
+    the input).  run() returns the output tensor on the owner, None elsewhere.
+    The host logic (partition, handle exchange, ordering) is plain
+    torch.distributed and runs under gloo as well."""
+
+    def __init__(self, img, levels: int, K: int, T: float, sigma_r: float, m: float, group=None, dst: int = 0):
+        import torch
+        import torch.distributed as dist
+
+        from . import fllf as F
+        self.F, self.dist, self.torch = F, dist, torch
+        self.group, self.dst = group, dst
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.img = img
+        C, H, W = img.shape
+        self.shape = (C, H, W)
+        self.device = img.device.index
+        nbytes = C * H * W * 4
+        if self.rank == dst:
+            self.ptr, handle = F.ipc_alloc(nbytes)
+            self.owned = True
+        else:
+            self.ptr, handle, self.owned = None, None, False
+        obj = [handle]
+        dist.broadcast_object_list(obj, src=dst, group=group)
+        if not self.owned:
+            self.ptr = F.ipc_open(obj[0])
+        self.out = F.device_view(self.ptr, (C, H, W), (H * W, W, 1), self.device)
+        runs = channel_runs(order_partition(C, K, self.world)[self.rank])
+        self.jobs = []
+        for r in runs:
+            p = F.Plan(H, W, levels, K, T, sigma_r, m, k_begin=r.k_begin, k_end=r.k_end,
+                       include_base=r.include_base, batch=r.nch)
+            self.jobs.append((r, p))
+
+    def run(self):
+        torch, dist, F = self.torch, self.dist, self.F
+        if self.owned:
+            self.out.zero_()
+            torch.cuda.synchronize()
+        dist.barrier(group=self.group)
+        for r, p in self.jobs:
+            src = self.img[r.channel:r.channel + r.nch]
+            p.build(src)
+            F.fllf_apply_accumulate(p.handle, self.out[r.channel:r.channel + r.nch])
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)
+        return self.out if self.owned else None
+
+    def close(self):
+        for _, p in self.jobs:
+            p.close()
+        self.jobs = []
+        if self.ptr is not None:
+            self.torch.cuda.synchronize()
+            (self.F.ipc_free if self.owned else self.F.ipc_close)(self.ptr)
+            self.ptr = None
+
+
 # ------------------------------------------------------------------ NEXT-1
 # Row-band split with per-level halo exchange (north star: "Large frames can
 # instead be split into row bands with halo exchange").  Every level of both

@@ -66,6 +66,11 @@ _SIGS = {
     "fllf_destroy": (ctypes.c_int, [_P]),
     "fllf_build_fourier_pyramids": (ctypes.c_int, [_P, _P, ctypes.c_size_t, _P]),
     "fllf_apply": (ctypes.c_int, [_P, ctypes.POINTER(fllf_apply_args), _P, ctypes.c_size_t, _P]),
+    "fllf_apply_accumulate": (ctypes.c_int, [_P, ctypes.POINTER(fllf_apply_args), _P, ctypes.c_size_t, _P]),
+    "fllf_ipc_alloc": (ctypes.c_int, [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p), _P]),
+    "fllf_ipc_free": (ctypes.c_int, [_P]),
+    "fllf_ipc_open": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_void_p)]),
+    "fllf_ipc_close": (ctypes.c_int, [_P]),
     "fllf_filter": (ctypes.c_int, [_P, _P, ctypes.c_size_t, _P, ctypes.c_size_t, _P]),
     "fllf_filter_host": (ctypes.c_int, [_P, _P, _P, _P]),
     "fllf_filter_host_frames": (ctypes.c_int, [_P, _P, ctypes.c_size_t, _P, ctypes.c_size_t, ctypes.c_int, _P]),
@@ -196,6 +201,41 @@ def fllf_apply(plan, out, mode=FLLF_SCALAR, a_k=None, sigma_map=None, m_map=None
         args.d_sigma_r, args.d_m, args.map_pitch_bytes = sp, mp, spitch
     _check(lib.fllf_apply(plan, ctypes.byref(args), optr, opitch, _stream_handle(stream)))
     del keep
+
+
+def fllf_apply_accumulate(plan, out, mode=FLLF_SCALAR, a_k=None, stream=None) -> None:
+    """As fllf_apply, but the level-0 result is atomically ADDED to `out` (which
+    may alias another process's buffer through fllf_ipc_open)."""
+    optr, opitch = _dev_image(out, "out")
+    args, keep = _apply_args(mode, a_k)
+    _check(lib.fllf_apply_accumulate(plan, ctypes.byref(args), optr, opitch, _stream_handle(stream)))
+    del keep
+
+
+IPC_HANDLE_BYTES = 64
+
+
+def ipc_alloc(nbytes: int):
+    """(device pointer, IPC handle bytes) of a fresh allocation on the current device."""
+    ptr = ctypes.c_void_p()
+    h = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+    _check(lib.fllf_ipc_alloc(int(nbytes), ctypes.byref(ptr), h))
+    return ptr.value, h.raw
+
+
+def ipc_free(ptr: int) -> None:
+    _check(lib.fllf_ipc_free(ptr))
+
+
+def ipc_open(handle: bytes) -> int:
+    """Map another process's allocation (its ipc_alloc handle) into this one."""
+    ptr = ctypes.c_void_p()
+    _check(lib.fllf_ipc_open(ctypes.create_string_buffer(bytes(handle), IPC_HANDLE_BYTES), ctypes.byref(ptr)))
+    return ptr.value
+
+
+def ipc_close(ptr: int) -> None:
+    _check(lib.fllf_ipc_close(ptr))
 
 
 def _apply_args(mode, a_k):
