@@ -141,6 +141,12 @@ def algorithmic_bytes(kind, level, dims, K, frames, levels):
     elif kind == "apply":
         has_d = level + 1 < lmax
         b = (8 + 8 * K) * N(level) + (8 * K + (4 if has_d else 0)) * N(level + 1)
+    elif kind == "fuse":
+        # design F: read G_l, Z_l; write G_{l+1}, Z_{l+1} and S_l
+        b = (4 + 8 * K) * (N(level) + N(level + 1)) + 4 * N(level)
+    elif kind == "collapse":
+        # D_l += up(D_{l+1}): read D_l, D_{l+1}; write D_l
+        b = 8 * N(level) + 4 * N(level + 1)
     else:
         b = 0
     return b * frames

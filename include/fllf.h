@@ -166,10 +166,21 @@ FLLF_API fllf_status fllf_ipc_free(void* d_ptr);
 FLLF_API fllf_status fllf_ipc_open(const void* handle, void** d_ptr);
 FLLF_API fllf_status fllf_ipc_close(void* d_ptr);
 
-/* build + apply(SCALAR) in one call (the common one-shot filter).  The launch
- * sequence is captured once into a CUDA graph (per plan, input/output buffer
- * pair and profiling flag) and replayed on `s`; FLLF_NO_GRAPH=1 in the
- * environment or fllf_plan_set_graphs(p, 0) launches the kernels directly. */
+/* build + apply(SCALAR) in one call (the common one-shot filter).  Full-frame
+ * plans with levels >= 3 run the materialise-once design F (DESIGN.md "Design
+ * F"): each level-l >= 1 build step also evaluates the level-l order sum of
+ * Eq. 14 from the rows it streams, so every pyramid plane of levels >= 1 is
+ * written once and read once (the "2K+1 pyramids" cost of P:262-263); the
+ * collapse (Eq. 4) follows over the real D planes, then the level-0 apply.
+ * The result equals build + apply up to fp32 rounding order; the pyramids
+ * (fllf_read_pyramid) are identical and a later fllf_apply on the plan works
+ * as after fllf_build_fourier_pyramids.  FLLF_NO_FUSE=1 in the environment
+ * (or an order count with no supported split) keeps the two-pass design AB.
+ * The launch sequence is captured once into a CUDA graph (per plan,
+ * input/output buffer pair and profiling flag) and replayed on `s`;
+ * FLLF_NO_GRAPH=1 in the environment or fllf_plan_set_graphs(p, 0) launches
+ * the kernels directly.  Row-band plans: FLLF_ERR_INVALID_ARGUMENT (use the
+ * per-level calls). */
 FLLF_API fllf_status fllf_filter(fllf_plan p, const float* d_img, size_t in_pitch_bytes, float* d_out,
                         size_t out_pitch_bytes, void* s);
 
@@ -307,7 +318,15 @@ FLLF_API int fllf_plan_last_launch_count(fllf_plan p);
  * fllf_plan_kernel_times synchronises those events and returns, per launch in
  * order: kind (FLLF_K_*), pyramid level (the fine level of the step) and the
  * duration in milliseconds; *count = number of records (<= capacity). */
-enum { FLLF_K_BUILD0 = 0, FLLF_K_BUILD = 1, FLLF_K_MAPBUILD = 2, FLLF_K_APPLY = 3, FLLF_K_APPLY0 = 4 };
+enum {
+  FLLF_K_BUILD0 = 0,   /* level-0 build (image -> G_1, Z_1)                                  */
+  FLLF_K_BUILD = 1,    /* build step l -> l+1, l >= 1                                        */
+  FLLF_K_MAPBUILD = 2, /* sigma_r / m map pyramids (MAPS)                                    */
+  FLLF_K_APPLY = 3,    /* apply level l >= 1 (design AB)                                     */
+  FLLF_K_APPLY0 = 4,   /* apply level 0 (+ collapse into the output)                         */
+  FLLF_K_FUSE = 5,     /* design F: build step l -> l+1 fused with the level-l order sum      */
+  FLLF_K_COLLAPSE = 6  /* design F: D_l += up(D_{l+1})                                        */
+};
 FLLF_API fllf_status fllf_plan_set_profiling(fllf_plan p, int enable);
 FLLF_API fllf_status fllf_plan_set_graphs(fllf_plan p, int enable);
 FLLF_API fllf_status fllf_plan_kernel_times(fllf_plan p, int capacity, int* kind, int* level,

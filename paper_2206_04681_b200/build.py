@@ -18,7 +18,7 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libfllf.so")
-SOURCES = ["fllf_host.cpp", "fllf_kernels.cu", "fllf_color.cu", "fllf_naive.cu"]
+SOURCES = ["fllf_host.cpp", "fllf_kernels.cu", "fllf_fused.cu", "fllf_color.cu", "fllf_naive.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -30,20 +30,32 @@ def nvcc() -> str:
 
 
 def build(verbose: bool = False, extra: list[str] | None = None, out: str | None = None) -> str:
+    """Compile every source to an object (in parallel), then link the shared
+    library; static cudart, exported symbols = the C ABI only."""
+    from concurrent.futures import ThreadPoolExecutor
+    import tempfile
     os.makedirs(LIBDIR, exist_ok=True)
     lib = out or LIB
-    srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-Xcompiler", "-fvisibility=hidden", "-I", INCLUDE, "-I", CSRC,
-           "-Xptxas", "-v" if verbose else "-O3", *srcs, "-o", lib, *(extra or [])]
-    # export only the C ABI (fllf_*): visibility=hidden + explicit default visibility
-    cmd += ["-DFLLF_BUILD"]
-    r = subprocess.run(cmd, capture_output=True, text=True)
-    if r.returncode != 0:
-        sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building libfllf.so")
-    if verbose:
-        sys.stderr.write(r.stderr)
+    common = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+              "-Xcompiler", "-fvisibility=hidden", "-I", INCLUDE, "-I", CSRC, "-DFLLF_BUILD", *(extra or [])]
+    with tempfile.TemporaryDirectory(prefix="fllf_build_") as tmp:
+        def compile_one(src: str) -> tuple[str, subprocess.CompletedProcess]:
+            obj = os.path.join(tmp, os.path.basename(src) + ".o")
+            cmd = [nvcc(), *common, "-Xptxas", "-v" if verbose else "-O3", "-c", os.path.join(CSRC, src), "-o", obj]
+            return obj, subprocess.run(cmd, capture_output=True, text=True)
+        with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+            results = list(ex.map(compile_one, SOURCES))
+        for (obj, r), src in zip(results, SOURCES):
+            if r.returncode != 0:
+                sys.stderr.write(r.stdout + r.stderr)
+                raise RuntimeError(f"nvcc failed compiling {src}")
+            if verbose:
+                sys.stderr.write(r.stderr)
+        cmd = [nvcc(), *ARCH, "-shared", "-o", lib, *[o for o, _ in results]]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("nvcc failed linking libfllf.so")
     return lib
 
 

@@ -1,0 +1,606 @@
+// Design F ("materialise once") kernels for sm_100a: the level-l order sum of
+// Eq. 14 fused into the build step l -> l+1 of Eq. 1,
+// plus the collapse of Eq. 4 over the real D planes.
+//
+// Design AB (fllf_kernels.cu) builds every pyramid first and then, coarse to
+// fine, re-reads Z_l and Z_{l+1} in the apply pass: each level >= 1 plane is
+// written once and read twice.  The paper's cost model is "the computing cost
+// of 2K+1 pyramids"; design F meets it by consuming Z_l while it
+// is streamed for the build:
+//
+//   k_fuse, level l >= 1 (one launch per level, fine to coarse):
+//     reads  G_l, Z_{l,k}                      (as k_build)
+//     writes G_{l+1}, Z_{l+1,k}                (as k_build)
+//     writes S_l = sum_k a_k Im(e^{-i k w_1 g} (Z_{l,k} - up Z_{l+1,k})),  g = G_l,
+//            into the D_l plane
+//   k_collapse, l = l_max-2 .. 1:  D_l += up(D_{l+1})   (D_{l_max-1} = S_{l_max-1})
+//   then the level-0 apply of design AB reads D_1 (k_apply_cl<LEVEL0>).
+//
+// D_l = O_l - G_l is the collapse from level l of the output pyramid minus
+// G_l; S_l is its level-l increment, so the two designs
+// compute the same D planes (exact algebra, different rounding order only).
+//
+// k_fuse layout.  CTA = one strip (R coarse rows x 28 coarse columns of one
+// frame) with NW = KL/NC "build" warps and 2 "sum" warps.  Build warp w owns
+// the NC orders [w NC, (w+1) NC) of the plan's order range; lane L holds
+// coarse column x = 28 cb + L - 2 and fine columns 2x, 2x+1 (reflect-101 per
+// lane at the frame borders).  It streams fine row pairs P_j = (2j, 2j+1),
+// j = o0-2 .. o0+R+1, through its own shared-memory ring (cp.async, PD pairs
+// ahead): the VERTICAL 5-tap with two rolling accumulators per order and
+// column, then the HORIZONTAL 5-tap on the finished coarse row from warp
+// shuffles (k_build's arithmetic, so G_{l+1} and Z_{l+1} are bit-identical to
+// design AB).  Lanes 1..30 hold valid coarse values; with the reflected fine
+// columns / rows those obey the up-sampling border rule (column -1 = x_1,
+// column C = x_{C-1} or x_{C-2}), so the coarse rows o0-1, o0+R and lanes 1, 30
+// are the up-sampling halo.  The last three coarse rows stay in registers,
+// and so do the Z_l values of the last three pairs; once coarse row i+1 is
+// finished the warp forms, for the 4 fine pixels of pair P_i per lane,
+//     V_k = Z_{l,k} - up(Z_{l+1,k})        (the complex Laplacian coefficient)
+// and writes it to a double-buffered shared array V[pair][k][row][col].  The
+// two sum warps (one per fine row of the pair; 2 pixels per lane) evaluate
+//     S = sum_k a_k Im(e^{-i k theta} V_k),   theta = w_1 g,
+// with Clenshaw's recurrence over ALL the plan's orders (one sincos per pixel,
+// no cross-warp reduction) and store S into D_l.  Named barriers FULL / EMPTY
+// per V buffer pace the producers and consumers.
+#include <cstdio>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <cstdlib>
+#include <algorithm>
+#include <atomic>
+
+#include "fllf_internal.h"
+#include "fllf_ptx.h"
+
+namespace fllf {
+namespace {
+
+#include "fllf_dev.h"
+
+constexpr int FUSE_COLS = 28;  // owned coarse columns per warp (lanes 2..29)
+constexpr int FUSE_BAR = 1;    // named barrier id of the batch hand-over
+
+// warps per CTA (one per NC-order chunk), bounded so that the CTA fits one
+// SM's register file at 128 registers per thread (16 warps = 4 per SMSP)
+constexpr int FUSE_MAX_WARPS = 16;
+// order-sum batch: NB fine row pairs = NB x 128 pixels, one per lane of the CTA
+__host__ __device__ inline int fuse_nb(int nw) { return nw >= 8 ? nw / 4 : 1; }
+
+__device__ __forceinline__ void bar_sync_id(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+// shared-memory accesses through 32-bit shared addresses
+__device__ __forceinline__ void cpa16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cpa8(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cpa4(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ float4 lds4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float2 lds2(uint32_t a) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float lds1(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts4(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void sts2(uint32_t a, float2 v) {
+  asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
+}
+
+// Shared-memory layout of one CTA (bytes), NB = fuse_nb(warps):
+//   C    [NB pairs][KL orders][2 fine rows][64 fine columns] float2   (NB x 1024 KL)
+//   Gb   [NB pairs][2 fine rows][64 fine columns] float                 (NB x 512)
+//   ring of warp 0:  DEPTH slots x (G 512 + Z 1024 NC)
+//   ring of warp w:  DEPTH slots x Z 1024 NC
+template <int NC, int PD>
+struct FuseLayout {
+  static constexpr int DEPTH = PD + 1;
+  static constexpr int ZSLOT = NC * 1024;  // NC orders x 2 rows x 32 lanes x float4
+  static constexpr int G0SLOT = 512 + ZSLOT;
+  __host__ __device__ static int g_off(int KL) { return fuse_nb(KL / NC) * KL * 1024; }
+  __host__ __device__ static int ring_off(int KL, int w) {
+    return g_off(KL) + fuse_nb(KL / NC) * 512 + (w == 0 ? 0 : DEPTH * G0SLOT + (w - 1) * DEPTH * ZSLOT);
+  }
+  __host__ __device__ static int smem(int KL) { return ring_off(KL, KL / NC); }
+};
+
+// Order sums (Eq. 14) of one batch of cnt fine row pairs (rows from row0):
+//   S = sum_k a_k Im(e^{-i k theta} V_k) = sum_k (c_cos,k cos k theta + c_sin,k sin k theta),
+// theta = w_1 g, from the coefficient pairs c_k in C and g in Gb, by
+// Clenshaw's recurrence (descending k: b_k = c_k + 2 cos theta b_{k+1} - b_{k+2};
+// see k_apply_cl), stored into D_l.  Pixel p = tid + j * nthreads of the
+// batch (pair q = p / 128, row r, fine column f).  Out of line: it runs once
+// per batch, and keeping it out of the unrolled stream loop keeps the hot
+// code in the instruction cache.
+__device__ __noinline__ void fuse_order_sum(const FuseParams& P, uint32_t sbase, int goff, float* dbase, int row0,
+                                            int cnt, int cb) {
+  const int KL = P.KL;
+  const int nthreads = blockDim.x;
+  const long long pitch = P.src.pitch;
+  const int Hf = P.Hf;
+#pragma unroll 1
+  for (int p = threadIdx.x; p < cnt * 128; p += nthreads) {
+    const int q = p >> 7, r = (p >> 6) & 1, f = p & 63;
+    const float g = lds1(sbase + goff + ((q * 2 + r) * 64 + f) * 4);
+    float sn, c1;
+    sincos_turns(g, P.invT, &sn, &c1);
+    const float2 tc = bc(2.f * c1);
+    float2 b1 = make_float2(0.f, 0.f), b2 = b1;
+    uint32_t a = sbase + ((q * KL + KL - 1) * 2 + r) * 512 + f * 8;
+    int k = KL;
+#pragma unroll 1
+    for (; k >= 4; k -= 4, a -= 4096) {
+      const float2 c3 = lds2(a), c2 = lds2(a - 1024), c1v = lds2(a - 2048), c0 = lds2(a - 3072);
+      b2 = pfma(tc, b1, padd(c3, pneg(b2)));
+      b1 = pfma(tc, b2, padd(c2, pneg(b1)));
+      b2 = pfma(tc, b1, padd(c1v, pneg(b2)));
+      b1 = pfma(tc, b2, padd(c0, pneg(b1)));
+    }
+#pragma unroll 1
+    for (; k > 0; --k, a -= 1024) {
+      const float2 nb2 = pfma(tc, b1, padd(lds2(a), pneg(b2)));
+      b2 = b1;
+      b1 = nb2;
+    }
+    // b1 = b_{k0}, b2 = b_{k0+1}
+    float res;
+    if (P.kbase == 1) {
+      res = fmaf(b1.x, c1, fmaf(b1.y, sn, -b2.x));
+    } else {
+      float sk, ck;
+      sincos_turns_n(g, P.invT, P.kbase, &sk, &ck);
+      const float cm = fmaf(ck, c1, sk * sn), sm = fmaf(sk, c1, -ck * sn);  // e^{i (k0-1) theta}
+      res = fmaf(b1.x, ck, fmaf(b1.y, sk, -fmaf(b2.x, cm, b2.y * sm)));
+    }
+    const int row = row0 + 2 * q + r;
+    const int col = 2 * (FUSE_COLS * cb - 2) + f;  // lanes 2..29 own f in [4, 60)
+    if (f >= 4 && f < 60 && col < P.Wf && row < Hf) {
+      float* sp = dbase + (long long)row * pitch + col;
+      FLLF_DBG_STORE(P, sp, 4);
+      *sp = res;
+    }
+  }
+}
+
+// ---- one warp: NC orders of the strip (DO_G: warp 0 also builds G;
+// ROWS_IN: no fine row of the strip needs reflection)
+template <int NC, int PD, bool EDGE, bool DO_G, bool ROWS_IN>
+struct FuseWarp {
+  using L = FuseLayout<NC, PD>;
+  static constexpr int DEPTH = L::DEPTH;
+  static constexpr int SLOT = DO_G ? L::G0SLOT : L::ZSLOT;
+  static constexpr int ZOFF = DO_G ? 512 : 0;
+
+  const FuseParams& P;
+  int o0, R, lane, warp, nw, nb;
+  int x, rc0, rc1, Hf;
+  bool store_lane, halo_l, halo_r;
+  long long zks, gpitch, zpitch;
+  const float* gsrc;    // G_l: next row pair (ROWS_IN) or the frame base
+  const float2* zsrc;   // Z_l, first order of the chunk: next row pair (ROWS_IN) or the frame base
+  float* gout;          // G_{l+1} at (o0 - 1, x): advanced one coarse row per emit
+  float2* zout;         // Z_{l+1} at (o0 - 1, x), first order of the chunk
+  uint32_t ring;        // this warp's ring (shared address)
+  uint32_t si, sr;      // ring slot offsets: next issue, next read
+  uint32_t crow;        // C[0][il0][0][2 lane] (shared address)
+  uint32_t gbrow;       // Gb[0][0][2 lane]
+  int jn;               // fine row pair of the next issue (reflected path)
+  float2 cwk[NC][4];    // this warp's Clenshaw coefficient pairs (ApplyParams::cw)
+  int cb_;
+  uint32_t sbase_;
+  float* dbase;         // D_l of the frame
+  float2 Pc[NC][2], Ac[NC][2];
+  float2 Pr, Ar;
+
+  __device__ __forceinline__ FuseWarp(const FuseParams& P_, int cb, int o0_, int R_, int frame, int nw_,
+                                      int warp_, uint32_t smem)
+      : P(P_), o0(o0_), R(R_), warp(warp_), nw(nw_) {
+    lane = threadIdx.x & 31;
+    nb = fuse_nb(nw);
+    Hf = P.Hf;
+    x = FUSE_COLS * cb + lane - 2;
+    const int c0 = 2 * x;
+    rc0 = EDGE ? refl101(c0, P.Wf) : c0;
+    rc1 = EDGE ? refl101(c0 + 1, P.Wf) : c0 + 1;
+    store_lane = lane >= 2 && lane <= 29 && x < P.Wc;
+    halo_l = EDGE && store_lane && x == 1;
+    halo_r = EDGE && store_lane && x == ((P.Wf & 1) ? P.Wc - 2 : P.Wc - 1);
+    const int il0 = warp * NC;
+    zks = P.src.kstride_z;
+    gpitch = P.src.pitch;
+    zpitch = P.src.zpitch;
+    const long long r0 = ROWS_IN ? 2LL * (o0 - 2) : 0;
+    gsrc = P.src.G + frame * P.src.fstride_r + r0 * gpitch + (EDGE ? 0 : c0);
+    zsrc = P.src.Z + frame * P.src.fstride_z + (long long)il0 * zks + r0 * zpitch + (EDGE ? 0 : c0);
+    gout = P.dst.G + frame * P.dst.fstride_r + (long long)(o0 - 1) * P.dst.pitch + x;
+    zout = P.dst.Z + frame * P.dst.fstride_z + (long long)il0 * P.dst.kstride_z + (long long)(o0 - 1) * P.dst.zpitch + x;
+    ring = smem + L::ring_off(P.KL, warp);
+    si = sr = 0;
+    crow = smem + il0 * 1024 + lane * 16;
+    gbrow = smem + L::g_off(P.KL) + lane * 8;
+    jn = o0 - 2;
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) cwk[i][u] = P.cw[il0 + i][u];
+      Pc[i][0] = Pc[i][1] = Ac[i][0] = Ac[i][1] = make_float2(0.f, 0.f);
+    }
+    Pr = Ar = make_float2(0.f, 0.f);
+    cb_ = cb;
+    sbase_ = smem;
+    dbase = P.src.D + frame * P.src.fstride_r;
+  }
+
+  // copies of the next pair (fine rows 2 jn, 2 jn + 1) into the next ring slot
+  __device__ __forceinline__ void issue() {
+    const uint32_t sl = ring + si;
+    si = si + SLOT == DEPTH * SLOT ? 0 : si + SLOT;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const float* gp;
+      const float2* zp;
+      if (ROWS_IN) {
+        gp = gsrc + r * gpitch;
+        zp = zsrc + r * zpitch;
+      } else {
+        const int rr = refl101(2 * jn + r, Hf);
+        gp = gsrc + rr * gpitch;
+        zp = zsrc + rr * zpitch;
+      }
+      if (DO_G) {
+        const uint32_t gd = sl + r * 256 + lane * 8;
+        if (EDGE) {
+          cpa4(gd, gp + rc0);
+          cpa4(gd + 4, gp + rc1);
+        } else {
+          cpa8(gd, gp);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < NC; ++i) {
+        const uint32_t zd = sl + ZOFF + (i * 2 + r) * 512 + lane * 16;
+        const float2* q = zp + i * zks;
+        if (EDGE) {
+          cpa8(zd, q + rc0);
+          cpa8(zd + 8, q + rc1);
+        } else {
+          cpa16(zd, q);
+        }
+      }
+    }
+    if (ROWS_IN) {
+      gsrc += 2 * gpitch;
+      zsrc += 2 * zpitch;
+    } else {
+      ++jn;
+    }
+  }
+
+  struct Pair {
+    float2 ge, go;
+    float4 ze[NC], zo[NC];
+  };
+  __device__ __forceinline__ void read(Pair& d) {
+    const uint32_t sl = ring + sr;
+    sr = sr + SLOT == DEPTH * SLOT ? 0 : sr + SLOT;
+    if (DO_G) {
+      d.ge = lds2(sl + lane * 8);
+      d.go = lds2(sl + 256 + lane * 8);
+    }
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      d.ze[i] = lds4(sl + ZOFF + (i * 2) * 512 + lane * 16);
+      d.zo[i] = lds4(sl + ZOFF + (i * 2 + 1) * 512 + lane * 16);
+    }
+  }
+
+  // finish the next coarse row from the even row of the current pair
+  // (k_build's arithmetic); OWN: store it
+  template <bool OWN>
+  __device__ __forceinline__ void emit(const Pair& d, float2 (&h)[NC]) {
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      const float2 ea = pfma(bc(W2), lo2(d.ze[i]), Pc[i][0]);
+      const float2 eb = pfma(bc(W2), hi2(d.ze[i]), Pc[i][1]);
+      h[i] = hfilt_c(ea, eb);
+      if (OWN) {
+        float2* q = zout + i * P.dst.kstride_z;
+        if (store_lane) {
+          FLLF_DBG_STORE(P, q, 8);
+          stg2(q, h[i]);
+        }
+        if (EDGE && halo_l) {
+          FLLF_DBG_STORE(P, q - 2, 8);
+          q[-2] = h[i];  // x == 1: column -1
+        }
+        if (EDGE && halo_r) {
+          FLLF_DBG_STORE(P, q + (P.Wc - x), 8);
+          q[P.Wc - x] = h[i];
+        }
+      }
+    }
+    if (DO_G) {
+      const float2 e = pfma(bc(W2), d.ge, Pr);
+      const float hg = hfilt_r(e.x, e.y);
+      if (OWN && store_lane) {
+        FLLF_DBG_STORE(P, gout, 4);
+        *gout = hg;
+      }
+      gout += P.dst.pitch;
+    }
+    zout += P.dst.zpitch;
+  }
+  __device__ __forceinline__ void vstep(const Pair& d) {
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      vstep_fixed(Pc[i][0], Ac[i][0], lo2(d.ze[i]), lo2(d.zo[i]));
+      vstep_fixed(Pc[i][1], Ac[i][1], hi2(d.ze[i]), hi2(d.zo[i]));
+    }
+    if (DO_G) vstep_fixed(Pr, Ar, d.ge, d.go);
+  }
+
+  // c_k = a_k (Im V_k, -Re V_k) with V_k = Z_{l,k} - up(Z_{l+1,k}) at the 4
+  // fine pixels of own pair n, from the coarse rows i-1, i, i+1 (Cm, C0, Cp)
+  // and the pair's Z_l values (ze, zo); at the end of a batch of NB pairs (or
+  // of the strip) the CTA evaluates the batch's order sums
+  __device__ __forceinline__ void coef(const float2 (&Cm)[NC], const float2 (&C0)[NC], const float2 (&Cp)[NC],
+                                       const float4 (&ze)[NC], const float4 (&zo)[NC], const float4& gg, int n,
+                                       int& q) {
+    const uint32_t cb = crow + q * (P.KL * 1024);
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      // vertical up-sampling (unscaled): even fine row x_{i-1} + 6 x_i + x_{i+1}, odd x_i + x_{i+1}
+      const float2 ve = pfma(bc(6.f), C0[i], padd(Cm[i], Cp[i]));
+      const float2 vo = padd(C0[i], Cp[i]);
+      const float2 veL = shfl_up2(ve), veR = shfl_down2(ve), voL = shfl_up2(vo), voR = shfl_down2(vo);
+      // horizontal + polyphase scales and a_k with the sign pattern (cwk)
+      const float2 c0 = pfma(pfma(bc(6.f), ve, padd(veL, veR)), cwk[i][0], pmul(lo2(ze[i]), cwk[i][3]));
+      const float2 c1 = pfma(padd(ve, veR), cwk[i][1], pmul(hi2(ze[i]), cwk[i][3]));
+      const float2 c2 = pfma(pfma(bc(6.f), vo, padd(voL, voR)), cwk[i][1], pmul(lo2(zo[i]), cwk[i][3]));
+      const float2 c3 = pfma(padd(vo, voR), cwk[i][2], pmul(hi2(zo[i]), cwk[i][3]));
+      sts4(cb + i * 1024, cat4(c0, c1));
+      sts4(cb + i * 1024 + 512, cat4(c2, c3));
+    }
+    if (DO_G) {  // g of the pair for the order sums
+      const uint32_t gb = gbrow + q * 512;
+      sts2(gb, lo2(gg));
+      sts2(gb + 256, hi2(gg));
+    }
+    if (++q == nb || n == R - 1) {
+      bar_sync_id(FUSE_BAR, nw * 32);  // the batch's C and g are complete
+      fuse_order_sum(P, sbase_, L::g_off(P.KL), dbase, 2 * (o0 + n + 1 - q), q, cb_);
+      bar_sync_id(FUSE_BAR, nw * 32);  // ... and consumed
+      q = 0;
+    }
+  }
+
+  // One step t (pair P_{o0-2+t}): Wm, W0 = coarse rows j-3, j-2; Wn <- row
+  // j-1 (emitted); De/Do/Dg <- this pair's Z_l (and G_l); Dm2 = pair j-2's.
+  template <bool EMIT, bool OWN, bool VSTEP, bool VC>
+  __device__ __forceinline__ void step(int t, int np, int& q, float2 (&Wm)[NC], float2 (&W0)[NC],
+                                       float2 (&Wn)[NC], float4 (&De)[NC], float4 (&Do)[NC], float4 (&Dg),
+                                       const float4 (&Dm2e)[NC], const float4 (&Dm2o)[NC], const float4& Dm2g) {
+    if (t + PD < np) issue();
+    cp_async_commit();
+    cp_async_wait<PD>();
+    Pair d;
+    read(d);
+    if (EMIT) emit<OWN>(d, Wn);
+    if (VSTEP) vstep(d);
+    if (VC) coef(Wm, W0, Wn, Dm2e, Dm2o, Dm2g, t - 4, q);
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      De[i] = d.ze[i];
+      Do[i] = d.zo[i];
+    }
+    if (DO_G) Dg = cat4(d.ge, d.go);
+  }
+
+  // Stream pairs P_{o0-2} .. P_{o0+R+1} (t = 0 .. R+3):
+  //   t = 0, 1: accumulate; t = 2: emit the halo row o0-1; t = 3: emit row o0;
+  //   t = 4 .. R+2: emit row o0-3+t, coefficients of own pair t-4;
+  //   t = R+3: emit the halo row o0+R, coefficients of the last own pair.
+  // The coarse window (rows j-3, j-2, j-1) and the delay line (pairs j-2,
+  // j-1, j) rotate with period 3 by renaming: phase t % 3 uses
+  //   0: (CB, CC -> CA; A <- pair, B = pair j-2)
+  //   1: (CC, CA -> CB; B <- pair, C = pair j-2)
+  //   2: (CA, CB -> CC; C <- pair, A = pair j-2)
+  __device__ __forceinline__ void run() {
+    const int np = R + 4;
+#pragma unroll
+    for (int i = 0; i < PD; ++i) {
+      if (i < np) issue();
+      cp_async_commit();
+    }
+    float2 CA[NC], CB[NC], CC[NC];
+    float4 ZAe[NC], ZAo[NC], ZBe[NC], ZBo[NC], ZCe[NC], ZCo[NC];
+    float4 GA = make_float4(0.f, 0.f, 0.f, 0.f), GB = GA, GC = GA;
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      CA[i] = CB[i] = CC[i] = make_float2(0.f, 0.f);
+      ZAe[i] = ZAo[i] = ZBe[i] = ZBo[i] = ZCe[i] = ZCo[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    int q = 0;
+#define FUSE_PH0 q, CB, CC, CA, ZAe, ZAo, GA, ZBe, ZBo, GB
+#define FUSE_PH1 q, CC, CA, CB, ZBe, ZBo, GB, ZCe, ZCo, GC
+#define FUSE_PH2 q, CA, CB, CC, ZCe, ZCo, GC, ZAe, ZAo, GA
+    step<false, false, true, false>(0, np, FUSE_PH0);
+    step<false, false, true, false>(1, np, FUSE_PH1);
+    step<true, false, true, false>(2, np, FUSE_PH2);
+    step<true, true, true, false>(3, np, FUSE_PH0);
+    int t = 4;
+#pragma unroll 1
+    for (; t + 2 <= R + 2; t += 3) {
+      step<true, true, true, true>(t, np, FUSE_PH1);
+      step<true, true, true, true>(t + 1, np, FUSE_PH2);
+      step<true, true, true, true>(t + 2, np, FUSE_PH0);
+    }
+    // 0..2 steady steps remain (phase 1 first), then the last step t = R+3
+    const int rem = R + 3 - t;
+    if (rem == 0) {
+      step<true, false, false, true>(t, np, FUSE_PH1);
+    } else if (rem == 1) {
+      step<true, true, true, true>(t, np, FUSE_PH1);
+      step<true, false, false, true>(t + 1, np, FUSE_PH2);
+    } else {
+      step<true, true, true, true>(t, np, FUSE_PH1);
+      step<true, true, true, true>(t + 1, np, FUSE_PH2);
+      step<true, false, false, true>(t + 2, np, FUSE_PH0);
+    }
+#undef FUSE_PH0
+#undef FUSE_PH1
+#undef FUSE_PH2
+    cp_async_wait<0>();
+  }
+};
+
+template <int NC, int PD, bool EDGE, bool ROWS_IN>
+__device__ __forceinline__ void fuse_run(const FuseParams& P, int cb, int o0, int R, int frame, int nw, int warp,
+                                         uint32_t sbase) {
+  if (warp == 0) {
+    FuseWarp<NC, PD, EDGE, true, ROWS_IN> w(P, cb, o0, R, frame, nw, warp, sbase);
+    w.run();
+  } else {
+    FuseWarp<NC, PD, EDGE, false, ROWS_IN> w(P, cb, o0, R, frame, nw, warp, sbase);
+    w.run();
+  }
+}
+
+template <int NC, int PD>
+__global__ void __launch_bounds__(FUSE_MAX_WARPS * 32, 1) k_fuse(const __grid_constant__ FuseParams P) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  pdl_wait();     // level l (G_l, Z_l) is complete
+  pdl_trigger();  // let the next level's kernel get scheduled
+  const uint32_t sbase = smem_u32(smem);
+  const int cb = blockIdx.x;
+  const int o0 = blockIdx.y * P.rows_per_strip;
+  const int R = min(P.rows_per_strip, P.Hc - o0);
+  const int frame = blockIdx.z;
+  const int nw = P.KL / NC;
+  const int warp = threadIdx.x >> 5;
+  // all 64 fine columns of the warp inside the row: no per-lane reflection
+  const bool interior = cb >= 1 && 2 * FUSE_COLS * cb + 60 <= P.Wf;
+  // pairs o0-2 .. o0+R+1 inside the frame: no row reflection
+  const bool rows_in = o0 >= 2 && 2 * (o0 + R + 1) + 1 < P.Hf;
+  if (interior) {
+    if (rows_in) fuse_run<NC, PD, false, true>(P, cb, o0, R, frame, nw, warp, sbase);
+    else fuse_run<NC, PD, false, false>(P, cb, o0, R, frame, nw, warp, sbase);
+  } else {
+    if (rows_in) fuse_run<NC, PD, true, true>(P, cb, o0, R, frame, nw, warp, sbase);
+    else fuse_run<NC, PD, true, false>(P, cb, o0, R, frame, nw, warp, sbase);
+  }
+}
+
+// D_l += up(D_{l+1}) (polyphase up-sampling with the border rule of upmap):
+// one thread per coarse pixel = a 2x2 block of fine pixels.
+__global__ void __launch_bounds__(128) k_collapse(const CollapseParams P) {
+  pdl_wait();  // D_{l+1} is complete
+  pdl_trigger();
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = blockIdx.y;
+  if (x >= P.Wc) return;
+  const float* dc = P.coarse + blockIdx.z * P.cfstride;
+  float* df = P.fine + blockIdx.z * P.ffstride;
+  const int xs[3] = {upmap(x - 1, P.Wc, P.Wf), x, upmap(x + 1, P.Wc, P.Wf)};
+  const int rs[3] = {upmap(r - 1, P.Hc, P.Hf), r, upmap(r + 1, P.Hc, P.Hf)};
+  float ve[3], vo[3];
+#pragma unroll
+  for (int b = 0; b < 3; ++b) {
+    const float d0 = __ldg(dc + (long long)rs[0] * P.cpitch + xs[b]);
+    const float d1 = __ldg(dc + (long long)rs[1] * P.cpitch + xs[b]);
+    const float d2 = __ldg(dc + (long long)rs[2] * P.cpitch + xs[b]);
+    ve[b] = fmaf(6.f, d1, d0 + d2) * 0.125f;
+    vo[b] = (d1 + d2) * 0.5f;
+  }
+  const float o[2][2] = {{fmaf(6.f, ve[1], ve[0] + ve[2]) * 0.125f, (ve[1] + ve[2]) * 0.5f},
+                         {fmaf(6.f, vo[1], vo[0] + vo[2]) * 0.125f, (vo[1] + vo[2]) * 0.5f}};
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const int row = 2 * r + t;
+    if (row >= P.Hf) break;
+    float* fp = df + (long long)row * P.fpitch + 2 * x;
+    if (2 * x + 1 < P.Wf) {
+      FLLF_DBG_STORE(P, fp, 8);
+      float2 v = *reinterpret_cast<float2*>(fp);
+      v.x += o[t][0];
+      v.y += o[t][1];
+      *reinterpret_cast<float2*>(fp) = v;
+    } else {
+      FLLF_DBG_STORE(P, fp, 4);
+      fp[0] += o[t][0];
+    }
+  }
+}
+
+constexpr int kFuseSmemMax = 227 * 1024;
+// ring depth (pairs ahead): 4 with one order per warp, 2 with two (shared memory)
+template <int NC>
+constexpr int fuse_pd() {
+  return NC == 1 ? 4 : 2;
+}
+
+template <int NC>
+cudaError_t launch_fuse_nc(const FuseParams& p0, int batch, cudaStream_t s, bool pdl) {
+  constexpr int PD = fuse_pd<NC>();
+  FuseParams p = p0;
+  const int bx = (p.Wc + FUSE_COLS - 1) / FUSE_COLS;
+  // strip height: long strips amortise the 8 halo fine rows (pairs o0-2,
+  // o0-1, o0+R, o0+R+1); shorter ones only while the grid would leave SMs idle
+  static const int rmax = [] {
+    const char* e = std::getenv("FLLF_FUSE_RMAX");
+    const int v = e ? std::atoi(e) : 64;
+    return v >= 1 ? v : 64;
+  }();
+  static const int target_ctas = [] {
+    const char* e = std::getenv("FLLF_FUSE_CTAS");
+    const int v = e ? std::atoi(e) : 148 * 4;
+    return v >= 1 ? v : 148 * 4;
+  }();
+  int R = std::min(rmax, p.Hc);
+  while (R > 4 && (long long)bx * ((p.Hc + R - 1) / R) * batch < target_ctas) R = (R + 1) / 2;
+  p.rows_per_strip = R;
+  const int smem = FuseLayout<NC, PD>::smem(p.KL);
+  static DeviceFlags attr_set;
+  cudaError_t e = smem_opt_in(k_fuse<NC, PD>, kFuseSmemMax, attr_set);
+  if (e != cudaSuccess) return e;
+  dim3 grid(bx, (p.Hc + R - 1) / R, batch);
+  return launch_ex(k_fuse<NC, PD>, grid, dim3(32 * (p.KL / NC)), smem, s, pdl, p);
+}
+
+}  // namespace
+
+int fuse_orders_per_warp(int KL) {
+  if (KL <= FUSE_MAX_WARPS && FuseLayout<1, fuse_pd<1>()>::smem(KL) <= kFuseSmemMax) return 1;
+  if (KL % 2 == 0 && KL / 2 <= FUSE_MAX_WARPS && FuseLayout<2, fuse_pd<2>()>::smem(KL) <= kFuseSmemMax) return 2;
+  return 0;
+}
+
+cudaError_t launch_fuse(const FuseParams& p, int batch, cudaStream_t s, bool pdl) {
+  switch (fuse_orders_per_warp(p.KL)) {
+    case 2: return launch_fuse_nc<2>(p, batch, s, pdl);
+    case 1: return launch_fuse_nc<1>(p, batch, s, pdl);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_collapse(const CollapseParams& p, int batch, cudaStream_t s, bool pdl) {
+  dim3 grid((p.Wc + 127) / 128, p.Hc, batch);
+  return launch_ex(k_collapse, grid, dim3(128), 0, s, pdl, p);
+}
+
+}  // namespace fllf

@@ -500,6 +500,9 @@ static fllf_status build_level_impl(fllf_plan p, const float* img, long long pit
 
 fllf_status fllf_build_fourier_pyramids(fllf_plan p, const float* d_img, size_t pitch_bytes, void* s) {
   if (!p) return fail(FLLF_ERR_BAD_POINTER, "NULL plan");
+  if (p->band)
+    return fail(FLLF_ERR_INVALID_ARGUMENT,
+                "build_fourier_pyramids: row-band plans need the per-level calls (halo exchange between levels)");
   long long pitch;
   fllf_status st = check_image(d_img, pitch_bytes, p->d.W, "build: d_img", &pitch);
   if (st != FLLF_OK) return st;
@@ -560,6 +563,18 @@ static fllf_status ensure_maps_ws(fllf_plan p) {
     p->lv[l].MM = p->lv[l].MS + p->lv[l].fstride_r;
   }
   return FLLF_OK;
+}
+
+// Clenshaw coefficient pairs of one order with coefficient a: the polyphase
+// up-sampling scales 1/64 (even row, even col), 1/16 (mixed), 1/4 (odd, odd)
+// and the same-level term, with the sign pattern of
+// Im(e^{-i k theta} V) = cos(k theta) V_im - sin(k theta) V_re folded in
+// (fllf::ApplyParams::cw).
+static void clenshaw_pairs(float a, float2 (&cw)[4]) {
+  cw[0] = make_float2(-a / 64.f, a / 64.f);
+  cw[1] = make_float2(-a / 16.f, a / 16.f);
+  cw[2] = make_float2(-a / 4.f, a / 4.f);
+  cw[3] = make_float2(a, -a);
 }
 
 // One apply level (coarse to fine; l = lmax-1 .. 0) with the prepared parameters.
@@ -626,7 +641,7 @@ static fllf_status apply_level_impl(fllf_plan p, fllf::ApplyParams& ap, int l, b
 // fllf_apply (only_level < 0: the whole coarse-to-fine pass) and
 // fllf_apply_level (only that level).
 static fllf_status apply_impl(fllf_plan p, const fllf_apply_args* a, float* d_out, size_t out_pitch_bytes, void* s,
-                              int only_level, bool accumulate = false) {
+                              int only_level, bool accumulate = false, bool chain_pdl = false) {
   if (!p) return fail(FLLF_ERR_BAD_POINTER, "NULL plan");
   if (!p->built) return fail(FLLF_ERR_NOT_BUILT, "fllf_apply before fllf_build_fourier_pyramids");
   long long opitch;
@@ -684,10 +699,7 @@ static fllf_status apply_impl(fllf_plan p, const fllf_apply_args* a, float* d_ou
     ap.wk[i][1] = make_float2(-ap.a[i] / 64.f, -ap.a[i] / 64.f);
     ap.wk[i][2] = make_float2(-ap.a[i] / 16.f, -ap.a[i] / 16.f);
     ap.wk[i][3] = make_float2(-ap.a[i] / 4.f, -ap.a[i] / 4.f);
-    ap.cw[i][0] = make_float2(-a / 64.f, a / 64.f);
-    ap.cw[i][1] = make_float2(-a / 16.f, a / 16.f);
-    ap.cw[i][2] = make_float2(-a / 4.f, a / 4.f);
-    ap.cw[i][3] = make_float2(a, -a);
+    clenshaw_pairs(a, ap.cw[i]);
   }
   int launches = 0;
   if (p->last_was_apply) p->nrec = 0;
@@ -742,7 +754,7 @@ static fllf_status apply_impl(fllf_plan p, const fllf_apply_args* a, float* d_ou
   const int lmax = p->nlev - 1;
   for (int l = lmax - 1; l >= 0; --l) {
     if (only_level >= 0 && l != only_level) continue;
-    st = apply_level_impl(p, ap, l, maps, stream, p->use_pdl && !p->band && only_level < 0);
+    st = apply_level_impl(p, ap, l, maps, stream, p->use_pdl && !p->band && (only_level < 0 || chain_pdl));
     if (st != FLLF_OK) return st;
     ++launches;
   }
@@ -751,6 +763,9 @@ static fllf_status apply_impl(fllf_plan p, const fllf_apply_args* a, float* d_ou
 }
 
 fllf_status fllf_apply(fllf_plan p, const fllf_apply_args* a, float* d_out, size_t out_pitch_bytes, void* s) {
+  if (p && p->band)
+    return fail(FLLF_ERR_INVALID_ARGUMENT,
+                "apply: row-band plans need the per-level calls (halo exchange between levels)");
   return apply_impl(p, a, d_out, out_pitch_bytes, s, -1);
 }
 
@@ -833,8 +848,103 @@ fllf_status fllf_plan_band_plane(fllf_plan p, int level, int kind, void** d_ptr,
   return FLLF_OK;
 }
 
+// Design F is used for full-frame plans with levels >= 3 whose order count has
+// a supported per-warp split, unless FLLF_NO_FUSE=1.
+static bool fuse_enabled(fllf_plan p) {
+  static const bool off = [] {
+    const char* e = std::getenv("FLLF_NO_FUSE");
+    return e && e[0] == '1';
+  }();
+  return !off && !p->band && p->nlev >= 3 && fllf::fuse_orders_per_warp(p->KL) > 0;
+}
+
+// Design F: build0; for l = 1 .. l_max-1 the fused
+// build step l -> l+1 + level-l order sum S_l (into D_l); the collapse
+// D_l += up(D_{l+1}) for l = l_max-2 .. 1; the level-0 apply (reads D_1).
+// All launches after the first are PDL-chained; each kernel waits for its
+// predecessor before it triggers the next one, so when a kernel starts every
+// kernel two or more places earlier has completed (the level-0 apply may
+// stage Z_1 before its own wait).
+static fllf_status filter_fused(fllf_plan p, const float* d_img, size_t in_pitch_bytes, float* d_out,
+                                size_t out_pitch_bytes, void* s) {
+  long long pitch;
+  fllf_status st = check_image(d_img, in_pitch_bytes, p->d.W, "filter: d_img", &pitch);
+  if (st != FLLF_OK) return st;
+  long long opitch;
+  st = check_image(d_out, out_pitch_bytes, p->d.W, "filter: d_out", &opitch);
+  if (st != FLLF_OK) return st;
+  DeviceGuard guard(p->device);
+  cudaStream_t stream = static_cast<cudaStream_t>(s);
+  const int lmax = p->nlev - 1;
+  const bool pdl = p->use_pdl;
+  p->nrec = 0;
+  p->last_was_apply = false;
+  int launches = 0;
+  st = build_level_impl(p, d_img, pitch, 0, stream, false);
+  if (st != FLLF_OK) return st;
+  ++launches;
+  fllf::FuseParams fp{};
+  {
+    std::vector<double> om(p->d.K), ak(p->d.K);
+    fllf_coefficients(p->d.K, p->d.T, p->d.sigma_r, p->d.m, om.data(), ak.data());
+    for (int i = 0; i < p->KL; ++i) clenshaw_pairs((float)ak[p->kb - 1 + i], fp.cw[i]);
+  }
+  fp.KL = p->KL;
+  fp.kbase = p->kb;
+  fp.invT = (float)(1.0 / p->d.T);
+  fp.dbg_lo = static_cast<const char*>(p->ws);
+  fp.dbg_hi = fp.dbg_lo + p->ws_bytes;
+  for (int l = 1; l < lmax; ++l) {
+    fp.src = p->lv[l];
+    fp.dst = p->lv[l + 1];
+    fp.Hf = p->Hs[l];
+    fp.Wf = p->Ws[l];
+    fp.Hc = p->Hs[l + 1];
+    fp.Wc = p->Ws[l + 1];
+    cudaError_t e;
+    {
+      ProfScope ps(p, stream, FLLF_K_FUSE, l);
+      e = fllf::launch_fuse(fp, p->d.batch, stream, pdl);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "fuse kernel launch");
+    ++launches;
+  }
+  for (int l = lmax - 2; l >= 1; --l) {
+    fllf::CollapseParams cp{};
+    const fllf::DevLevel& F = p->lv[l];
+    const fllf::DevLevel& C = p->lv[l + 1];
+    cp.coarse = C.D;
+    cp.cpitch = C.pitch;
+    cp.cfstride = C.fstride_r;
+    cp.fine = F.D;
+    cp.fpitch = F.pitch;
+    cp.ffstride = F.fstride_r;
+    cp.Hf = F.H;
+    cp.Wf = F.W;
+    cp.Hc = C.H;
+    cp.Wc = C.W;
+    cp.dbg_lo = static_cast<const char*>(p->ws);
+    cp.dbg_hi = cp.dbg_lo + p->ws_bytes;
+    cudaError_t e;
+    {
+      ProfScope ps(p, stream, FLLF_K_COLLAPSE, l);
+      e = fllf::launch_collapse(cp, p->d.batch, stream, pdl);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "collapse kernel launch");
+    ++launches;
+  }
+  p->built = true;
+  p->img = d_img;
+  p->img_pitch = pitch;
+  st = apply_impl(p, nullptr, d_out, out_pitch_bytes, s, 0, false, true);
+  if (st != FLLF_OK) return st;
+  p->last_launches = launches + 1;
+  return FLLF_OK;
+}
+
 static fllf_status filter_eager(fllf_plan p, const float* d_img, size_t in_pitch_bytes, float* d_out,
                                 size_t out_pitch_bytes, void* s) {
+  if (fuse_enabled(p)) return filter_fused(p, d_img, in_pitch_bytes, d_out, out_pitch_bytes, s);
   fllf_status st = fllf_build_fourier_pyramids(p, d_img, in_pitch_bytes, s);
   if (st != FLLF_OK) return st;
   const int nb = p->last_launches;
@@ -846,6 +956,8 @@ static fllf_status filter_eager(fllf_plan p, const float* d_img, size_t in_pitch
 fllf_status fllf_filter(fllf_plan p, const float* d_img, size_t in_pitch_bytes, float* d_out,
                         size_t out_pitch_bytes, void* s) {
   if (!p) return fail(FLLF_ERR_BAD_POINTER, "NULL plan");
+  if (p->band)
+    return fail(FLLF_ERR_INVALID_ARGUMENT, "filter: row-band plans need the per-level calls (halo exchange)");
   if (!p->use_graph) return filter_eager(p, d_img, in_pitch_bytes, d_out, out_pitch_bytes, s);
   DeviceGuard guard(p->device);
   fllf_plan_s::GraphEntry* g = nullptr;

@@ -115,6 +115,37 @@ struct ApplyParams {
   const char* dbg_hi;
 };
 
+// Materialise-once design F (fllf_fused.cu).  One
+// launch per level l >= 1 builds level l+1 from level l (G_{l+1}, Z_{l+1}, as
+// k_build) AND evaluates the level-l order sum
+//   S_l = sum_k a_k Im(e^{-i w_k g} (Z_{l,k} - up Z_{l+1,k})),  g = G_l,
+// from the same staged rows, storing S_l into the D_l plane; every Z plane
+// is then written once and read once.
+struct FuseParams {
+  DevLevel src;        // level l: G_l, Z_l read; S_l written to src.D
+  DevLevel dst;        // level l+1: G_{l+1}, Z_{l+1} written
+  int Hf, Wf, Hc, Wc;  // dims of levels l and l+1
+  int KL, kbase;       // local orders, global order of local order 0
+  int rows_per_strip;  // coarse rows per CTA
+  float invT;          // 1/T
+  // Clenshaw coefficient pairs per local order, as ApplyParams::cw
+  float2 cw[FLLF_MAX_K][4];
+  const char* dbg_lo;  // FLLF_DEBUG_BOUNDS builds: every global store must land in [dbg_lo, dbg_hi)
+  const char* dbg_hi;
+};
+
+// Collapse step of design F: fine += up(coarse) on the D planes of two
+// consecutive levels (D_l = S_l + up(D_{l+1}); Eq. 4).
+struct CollapseParams {
+  const float* coarse;  // D_{l+1}
+  long long cpitch, cfstride;
+  float* fine;          // D_l (in place)
+  long long fpitch, ffstride;
+  int Hf, Wf, Hc, Wc;
+  const char* dbg_lo;
+  const char* dbg_hi;
+};
+
 // Colour conversion (fllf_color.cu): three planes in, three planes out, all
 // with the same row pitch (floats).
 struct ColorParams {
@@ -164,5 +195,11 @@ cudaError_t launch_collapse_up(float* fine, long long fpitch, const float* coars
 cudaError_t launch_build(const BuildParams& p, int level_src, int batch, cudaStream_t s, bool pdl);
 cudaError_t launch_apply(const ApplyParams& p, int level_fine, bool has_d, bool maps, int batch,
                          cudaStream_t s, bool pdl);
+
+// Design F (fllf_fused.cu).  fuse_orders_per_warp: the order chunk per warp
+// for KL local orders (0: no supported split, the caller keeps design AB).
+int fuse_orders_per_warp(int KL);
+cudaError_t launch_fuse(const FuseParams& p, int batch, cudaStream_t s, bool pdl);
+cudaError_t launch_collapse(const CollapseParams& p, int batch, cudaStream_t s, bool pdl);
 
 }  // namespace fllf

@@ -41,6 +41,7 @@
 #include <stdint.h>
 #include <cstdlib>
 #include <algorithm>
+#include <atomic>
 
 #include "fllf_internal.h"
 #include "fllf_ptx.h"
@@ -48,131 +49,8 @@
 namespace fllf {
 namespace {
 
-constexpr unsigned FULL = 0xffffffffu;
+#include "fllf_dev.h"  // device helpers shared with fllf_fused.cu
 
-// Debug-bounds builds (`build --variant dbg -DFLLF_DEBUG_BOUNDS`; compute-
-// sanitizer is closed on this GPU pool): every global store of the pyramid
-// kernels is checked against the range the host declared for the launch
-// (the plan workspace, or the caller's output) and traps on a miss.
-#ifdef FLLF_DEBUG_BOUNDS
-#define FLLF_DBG_STORE(P, ptr, nbytes)                                                                       \
-  do {                                                                                                      \
-    const char* p_ = reinterpret_cast<const char*>(ptr);                                                   \
-    if (p_ < (P).dbg_lo || p_ + (nbytes) > (P).dbg_hi) {                                                    \
-      printf("fllf bounds: line %d block (%d,%d,%d) thread %d\n", __LINE__, blockIdx.x, blockIdx.y,        \
-             blockIdx.z, threadIdx.x);                                                                      \
-      __trap();                                                                                             \
-    }                                                                                                       \
-  } while (0)
-#else
-#define FLLF_DBG_STORE(P, ptr, nbytes) ((void)0)
-#endif
-// [1,4,6,4,1]/16
-constexpr float W0 = 0.375f, W1 = 0.25f, W2 = 0.0625f;
-constexpr float TWO_PI = 6.28318530717958647692f;
-
-// ------------------------------------------------------------- helpers
-__device__ __forceinline__ float2 bc(float w) { return make_float2(w, w); }
-__device__ __forceinline__ float2 pfma(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
-__device__ __forceinline__ float2 pmul(float2 a, float2 b) { return __fmul2_rn(a, b); }
-__device__ __forceinline__ float2 padd(float2 a, float2 b) { return __fadd2_rn(a, b); }
-__device__ __forceinline__ float2 pneg(float2 a) { return make_float2(-a.x, -a.y); }
-__device__ __forceinline__ float2 lo2(float4 v) { return make_float2(v.x, v.y); }
-__device__ __forceinline__ float2 hi2(float4 v) { return make_float2(v.z, v.w); }
-__device__ __forceinline__ float4 cat4(float2 a, float2 b) { return make_float4(a.x, a.y, b.x, b.y); }
-
-__device__ __forceinline__ float2 shfl_up2(float2 v) {
-  return make_float2(__shfl_up_sync(FULL, v.x, 1), __shfl_up_sync(FULL, v.y, 1));
-}
-__device__ __forceinline__ float2 shfl_down2(float2 v) {
-  return make_float2(__shfl_down_sync(FULL, v.x, 1), __shfl_down_sync(FULL, v.y, 1));
-}
-
-// Reflect-101 (reading R2) for indices within one bounce; clamps beyond (those
-// lanes only feed halo values that are never stored).
-__device__ __forceinline__ int refl101(int i, int n) {
-  i = i < 0 ? -i : i;
-  i = i >= n ? 2 * (n - 1) - i : i;
-  return min(max(i, 0), n - 1);
-}
-
-// Coarse index used by the polyphase up-sampling at fine size nf (coarse
-// C = ceil(nf/2)), equivalent to reflect-101 on the zero-inserted fine grid:
-// x_{-1} := x_1; x_C := x_{C-1} if nf is even, x_{C-2} if nf is odd.
-__device__ __forceinline__ int upmap(int c, int C, int nf) {
-  if (c < 0) c = -c;
-  if (c >= C) c = (c == C) ? ((nf & 1) ? C - 2 : C - 1) : C - 1;
-  return min(c, C - 1);
-}
-
-// theta = w_1 * val = 2 pi * frac(val / T): range-reduced in turns first.
-__device__ __forceinline__ void sincos_turns(float val, float invT, float* s, float* c) {
-  float u = val * invT;
-  u -= rintf(u);
-  __sincosf(TWO_PI * u, s, c);
-}
-
-// e^{i n theta}: n * frac(val/T) reduced again to [-1/2, 1/2] turns.
-__device__ __forceinline__ void sincos_turns_n(float val, float invT, int n, float* s, float* c) {
-  float u = val * invT;
-  u -= rintf(u);
-  u *= (float)n;
-  u -= rintf(u);
-  __sincosf(TWO_PI * u, s, c);
-}
-
-// complex products for unit phasors.  (s, c) layout = (Im, Re).
-__device__ __forceinline__ float2 cmul_sc(float2 a, float2 b) {
-  return make_float2(fmaf(a.x, b.y, a.y * b.x), fmaf(a.y, b.y, -a.x * b.x));
-}
-// (c, s) layout = (Re, Im).
-__device__ __forceinline__ float2 cmul_cs(float2 a, float2 b) {
-  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
-}
-// global store of a float2 (the address came through inline PTX, so say "global")
-__device__ __forceinline__ void stg2(float2* q, float2 v) {
-  asm volatile("st.global.v2.f32 [%0], {%1, %2};" ::"l"(q), "f"(v.x), "f"(v.y) : "memory");
-}
-// base + off (float2 elements, 32-bit unsigned offset) as one IMAD.WIDE.U32
-__device__ __forceinline__ float2* wide_off(float2* base, unsigned off) {
-  float2* r;
-  asm("mad.wide.u32 %0, %1, 8, %2;" : "=l"(r) : "r"(off), "l"(base));
-  return r;
-}
-__device__ __forceinline__ float2 ldg2(const float* p) { return __ldg(reinterpret_cast<const float2*>(p)); }
-__device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
-__device__ __forceinline__ float4 ldg4(const float2* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
-
-// One vertical step over a row pair (even row 2o, odd row 2o+1) for one
-// packed value: Pv holds output o-1 missing its last tap, Av output o.
-// After the step the roles swap (new P = Av, new A = Pv):
-//   Av += w0 ve + w1 vo ;  Pv = w2 ve + w1 vo.
-__device__ __forceinline__ void vstep(float2& Pv, float2& Av, float2 ve, float2 vo) {
-  Av = pfma(bc(W1), vo, pfma(bc(W0), ve, Av));
-  Pv = pfma(bc(W1), vo, pmul(bc(W2), ve));
-}
-
-// Same step with fixed names: P = pending output o-1 (missing its last tap),
-// A = output o.  After the pair: P <- A + w0 ve + w1 vo (output o, missing its
-// last tap), A <- w2 ve + w1 vo (output o+1).
-__device__ __forceinline__ void vstep_fixed(float2& Pv, float2& Av, float2 ve, float2 vo) {
-  Pv = pfma(bc(W1), vo, pfma(bc(W0), ve, Av));
-  Av = pfma(bc(W1), vo, pmul(bc(W2), ve));
-}
-
-// Horizontal 5-tap + decimation of a finished complex row value held as
-// (a, b) = (fine col 2x, 2x+1), each (Im, Re):
-//   h(x) = w2 f(2x-2) + w1 f(2x-1) + w0 f(2x) + w1 f(2x+1) + w2 f(2x+2)
-__device__ __forceinline__ float2 hfilt_c(float2 a, float2 b) {
-  const float2 pa = shfl_up2(a), pb = shfl_up2(b), na = shfl_down2(a);
-  return pfma(bc(W0), a, pfma(bc(W1), padd(pb, b), pmul(bc(W2), padd(pa, na))));
-}
-__device__ __forceinline__ float hfilt_r(float a, float b) {
-  const float pa = __shfl_up_sync(FULL, a, 1);
-  const float pb = __shfl_up_sync(FULL, b, 1);
-  const float na = __shfl_down_sync(FULL, a, 1);
-  return fmaf(W2, pa + na, fmaf(W1, pb + b, W0 * a));
-}
 
 // ----------------------------------------------------------------- build
 // One warp = 30 coarse output columns x a strip of R output rows, for NC
@@ -1698,20 +1576,6 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0, MAPS>()) k_apply_cl
   }
 }
 
-template <typename Kern, typename... Args>
-cudaError_t launch_ex(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl, const Args&... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, kern, args...);
-}
 
 // Rows per warp strip: long strips amortise the 3 halo rows; shorter strips
 // only when the grid would leave SMs without warps.
@@ -1808,14 +1672,6 @@ cudaError_t launch_build(const BuildParams& p0, int level_src, int batch, cudaSt
   }
 }
 
-static int sm_count() {
-  static int n = [] {
-    int dev = 0, v = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v;
-  }();
-  return n;
-}
 
 template <bool L0, bool HD, bool MP>
 static cudaError_t launch_apply_t(const ApplyParams& p, int batch, cudaStream_t s, bool pdl) {
@@ -1823,12 +1679,9 @@ static cudaError_t launch_apply_t(const ApplyParams& p, int batch, cudaStream_t 
   const int per_sm = MP ? 2 : 3;  // resident CTAs per SM (launch bounds)
   dim3 grid(std::min(ntiles, sm_count() * per_sm));
   const int smem = apply_stages<L0>() * apply_stage_bytes<L0>();
-  static bool attr_set = false;  // > 48 KB of dynamic shared memory needs an opt-in
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_apply<L0, HD, MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static DeviceFlags attr_set;  // > 48 KB of dynamic shared memory needs an opt-in, per device
+  cudaError_t e = smem_opt_in(k_apply<L0, HD, MP>, smem, attr_set);
+  if (e != cudaSuccess) return e;
   return launch_ex(k_apply<L0, HD, MP>, grid, dim3(160), smem, s, pdl, p, ntiles);
 }
 
@@ -1837,12 +1690,9 @@ static cudaError_t launch_apply_cl_t(const ApplyParams& p, int batch, cudaStream
   const int ntiles = ((p.Wf + 119) / 120) * ((p.r_end - p.r_begin + 3) / 4) * batch;
   dim3 grid(std::min(ntiles, sm_count() * apply_cl_ctas<L0, MP>()));
   const int smem = apply_cl_smem<L0, MP>();
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_apply_cl<L0, HD, MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static DeviceFlags attr_set;
+  cudaError_t e = smem_opt_in(k_apply_cl<L0, HD, MP>, smem, attr_set);
+  if (e != cudaSuccess) return e;
   return launch_ex(k_apply_cl<L0, HD, MP>, grid, dim3(160), smem, s, pdl, p, ntiles);
 }
 

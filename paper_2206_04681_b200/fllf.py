@@ -456,7 +456,7 @@ def fllf_naive_llf(plan, img, out, remap_mode=REMAP_EXACT, stream=None) -> None:
     _check(lib.fllf_naive_llf(plan, ip, ipitch, int(remap_mode), op, opitch, _stream_handle(stream)))
 
 
-KERNEL_KINDS = {0: "build0", 1: "build", 2: "mapbuild", 3: "apply", 4: "apply0"}
+KERNEL_KINDS = {0: "build0", 1: "build", 2: "mapbuild", 3: "apply", 4: "apply0", 5: "fuse", 6: "collapse"}
 
 
 def fllf_plan_set_profiling(plan, enable: bool) -> None:
