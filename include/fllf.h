@@ -301,6 +301,9 @@ FLLF_API fllf_status fllf_plan_band_plane(fllf_plan p, int level, int kind, void
                                           int* first_row, int* rows, int* planes, size_t* plane_stride_bytes);
 
 /* Introspection (tests, tooling). */
+/* The plan's effective description: defaults resolved (k_begin/k_end of the
+ * full range, row_end = H without a band, device = the plan's ordinal). */
+FLLF_API fllf_status fllf_plan_get_desc(fllf_plan p, fllf_plan_desc* out);
 FLLF_API fllf_status fllf_plan_level_dims(fllf_plan p, int level, int* H, int* W);
 FLLF_API fllf_status fllf_workspace_bytes(fllf_plan p, size_t* bytes);
 /* Copy one built pyramid plane (levels 1..l_max) of one frame to d_dst:
@@ -328,6 +331,19 @@ enum {
   FLLF_K_COLLAPSE = 6  /* design F: D_l += up(D_{l+1})                                        */
 };
 FLLF_API fllf_status fllf_plan_set_profiling(fllf_plan p, int enable);
+/* Which design fllf_filter runs:
+ *   FLLF_DESIGN_AUTO (default): design F on the pyramid levels l >= 1 whose
+ *     pixel count over the batch is >= 4 MP (FLLF_FUSE_MIN_MP in the
+ *     environment overrides), design AB on the coarser ones;
+ *   FLLF_DESIGN_AB: build + apply everywhere;
+ *   FLLF_DESIGN_F: design F on every level it supports.
+ * Results agree to fp32 rounding.  INVALID_ARGUMENT for other values. */
+enum { FLLF_DESIGN_AUTO = 0, FLLF_DESIGN_AB = 1, FLLF_DESIGN_F = 2 };
+FLLF_API fllf_status fllf_plan_set_design(fllf_plan p, int design);
+/* Finer control of the same choice: design F on levels 1 .. n (n >= 1; n is
+ * clamped to l_max-1), design AB above; n = 0 restores FLLF_DESIGN_AUTO.
+ * INVALID_ARGUMENT for n < 0. */
+FLLF_API fllf_status fllf_plan_set_fused_levels(fllf_plan p, int n);
 FLLF_API fllf_status fllf_plan_set_graphs(fllf_plan p, int enable);
 FLLF_API fllf_status fllf_plan_kernel_times(fllf_plan p, int capacity, int* kind, int* level,
                                             float* ms, int* count);

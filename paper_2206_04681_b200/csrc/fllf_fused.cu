@@ -383,7 +383,7 @@ struct FuseWarp {
     }
     if (++q == nb || n == R - 1) {
       bar_sync_id(FUSE_BAR, nw * 32);  // the batch's C and g are complete
-      fuse_order_sum(P, sbase_, L::g_off(P.KL), dbase, 2 * (o0 + n + 1 - q), q, cb_);
+      if (!(P.exp & 1)) fuse_order_sum(P, sbase_, L::g_off(P.KL), dbase, 2 * (o0 + n + 1 - q), q, cb_);
       bar_sync_id(FUSE_BAR, nw * 32);  // ... and consumed
       q = 0;
     }
@@ -402,7 +402,13 @@ struct FuseWarp {
     read(d);
     if (EMIT) emit<OWN>(d, Wn);
     if (VSTEP) vstep(d);
-    if (VC) coef(Wm, W0, Wn, Dm2e, Dm2o, Dm2g, t - 4, q);
+    if (VC) {
+      if (P.exp & 2) {
+        if (++q == nb || t - 4 == R - 1) q = 0;
+      } else {
+        coef(Wm, W0, Wn, Dm2e, Dm2o, Dm2g, t - 4, q);
+      }
+    }
 #pragma unroll
     for (int i = 0; i < NC; ++i) {
       De[i] = d.ze[i];
@@ -549,9 +555,12 @@ __global__ void __launch_bounds__(128) k_collapse(const CollapseParams P) {
 
 constexpr int kFuseSmemMax = 227 * 1024;
 // ring depth (pairs ahead): 4 with one order per warp, 2 with two (shared memory)
+#ifndef FLLF_FUSE_PD1
+#define FLLF_FUSE_PD1 4
+#endif
 template <int NC>
 constexpr int fuse_pd() {
-  return NC == 1 ? 4 : 2;
+  return NC == 1 ? FLLF_FUSE_PD1 : 2;
 }
 
 template <int NC>
@@ -574,6 +583,11 @@ cudaError_t launch_fuse_nc(const FuseParams& p0, int batch, cudaStream_t s, bool
   int R = std::min(rmax, p.Hc);
   while (R > 4 && (long long)bx * ((p.Hc + R - 1) / R) * batch < target_ctas) R = (R + 1) / 2;
   p.rows_per_strip = R;
+  static const int exp = [] {  // A/B experiments: 1 = no order sums, 2 = no coefficients (timing only)
+    const char* e = std::getenv("FLLF_FUSE_EXP");
+    return e ? std::atoi(e) : 0;
+  }();
+  p.exp = exp;
   const int smem = FuseLayout<NC, PD>::smem(p.KL);
   static DeviceFlags attr_set;
   cudaError_t e = smem_opt_in(k_fuse<NC, PD>, kFuseSmemMax, attr_set);

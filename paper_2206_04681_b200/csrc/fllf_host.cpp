@@ -91,6 +91,8 @@ struct fllf_plan_s {
   // caller's stream; re-captured when the buffers or the profiling flag change
   bool use_graph = true;
   bool use_pdl = true;  // programmatic dependent launch between the kernels of a sequence
+  int design = FLLF_DESIGN_AUTO;  // fllf_plan_set_design
+  int fused_levels = 0;           // fllf_plan_set_fused_levels (0: by design)
   bool capturing = false;
   cudaStream_t cap_stream = nullptr;
   struct GraphEntry {
@@ -108,6 +110,7 @@ struct fllf_plan_s {
   unsigned long long graph_clock = 0;
   // fllf_filter_host_frames: double-buffered device staging and the copy streams
   static constexpr int kPipe = 2;  // staging slots (double-buffered; 3 measured no faster)
+  bool pipe_ready = false;  // every staging buffer, stream and event below exists
   float* pipe_in[kPipe] = {};
   float* pipe_out[kPipe] = {};
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
@@ -421,6 +424,8 @@ fllf_status fllf_plan_create_ex(const fllf_plan_desc* din, fllf_plan* out) {
   return FLLF_OK;
 }
 
+static void pipe_release(fllf_plan p);
+
 fllf_status fllf_destroy(fllf_plan p) {
   if (!p) return FLLF_OK;
   {
@@ -435,16 +440,7 @@ fllf_status fllf_destroy(fllf_plan p) {
     for (cudaEvent_t e : p->ev_stop) cudaEventDestroy(e);
     for (auto& g : p->graphs)
       if (g.exec) cudaGraphExecDestroy(g.exec);
-    for (int i = 0; i < fllf_plan_s::kPipe; ++i) {
-      if (p->pipe_in[i]) cudaFree(p->pipe_in[i]);
-      if (p->pipe_out[i]) cudaFree(p->pipe_out[i]);
-      for (cudaEvent_t ev : {p->ev_in[i], p->ev_done[i], p->ev_out[i]})
-        if (ev) cudaEventDestroy(ev);
-    }
-    if (p->s_h2d) cudaStreamDestroy(p->s_h2d);
-    if (p->s_d2h) cudaStreamDestroy(p->s_d2h);
-    if (p->ev_pstart) cudaEventDestroy(p->ev_pstart);
-    if (p->ev_pend) cudaEventDestroy(p->ev_pend);
+    pipe_release(p);
     if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
     cudaGetLastError();
   }
@@ -638,10 +634,11 @@ static fllf_status apply_level_impl(fllf_plan p, fllf::ApplyParams& ap, int l, b
   return e == cudaSuccess ? FLLF_OK : cuda_fail(e, "apply kernel launch");
 }
 
-// fllf_apply (only_level < 0: the whole coarse-to-fine pass) and
-// fllf_apply_level (only that level).
+// Apply levels hi down to lo (coarse to fine): fllf_apply (lo = 0, hi = l_max-1),
+// fllf_apply_level (lo = hi = level) and design F's AB levels / level 0
+// (chain_pdl: PDL-linked to the launches before it).
 static fllf_status apply_impl(fllf_plan p, const fllf_apply_args* a, float* d_out, size_t out_pitch_bytes, void* s,
-                              int only_level, bool accumulate = false, bool chain_pdl = false) {
+                              int lo, int hi, bool accumulate = false, bool chain_pdl = false) {
   if (!p) return fail(FLLF_ERR_BAD_POINTER, "NULL plan");
   if (!p->built) return fail(FLLF_ERR_NOT_BUILT, "fllf_apply before fllf_build_fourier_pyramids");
   long long opitch;
@@ -651,8 +648,9 @@ static fllf_status apply_impl(fllf_plan p, const fllf_apply_args* a, float* d_ou
   if (mode != FLLF_SCALAR && mode != FLLF_COEFFS && mode != FLLF_MAPS)
     return fail(FLLF_ERR_INVALID_ARGUMENT, "apply: unknown mode");
   if (mode == FLLF_MAPS && p->band) return fail(FLLF_ERR_INVALID_ARGUMENT, "apply(MAPS) is not supported on row bands");
-  if (only_level >= 0 && mode == FLLF_MAPS) return fail(FLLF_ERR_INVALID_ARGUMENT, "apply_level: MAPS not supported");
-  if (only_level >= p->nlev - 1) return fail(FLLF_ERR_INVALID_ARGUMENT, "apply_level: level out of range");
+  const bool partial = !(lo == 0 && hi == p->nlev - 2);
+  if (partial && mode == FLLF_MAPS) return fail(FLLF_ERR_INVALID_ARGUMENT, "apply_level: MAPS not supported");
+  if (lo < 0 || hi >= p->nlev - 1 || lo > hi) return fail(FLLF_ERR_INVALID_ARGUMENT, "apply_level: level out of range");
   DeviceGuard guard(p->device);
   cudaStream_t stream = static_cast<cudaStream_t>(s);
   const double T = p->d.T;
@@ -752,9 +750,8 @@ static fllf_status apply_impl(fllf_plan p, const fllf_apply_args* a, float* d_ou
     }
   }
   const int lmax = p->nlev - 1;
-  for (int l = lmax - 1; l >= 0; --l) {
-    if (only_level >= 0 && l != only_level) continue;
-    st = apply_level_impl(p, ap, l, maps, stream, p->use_pdl && !p->band && (only_level < 0 || chain_pdl));
+  for (int l = hi; l >= lo; --l) {
+    st = apply_level_impl(p, ap, l, maps, stream, p->use_pdl && !p->band && (!partial || chain_pdl));
     if (st != FLLF_OK) return st;
     ++launches;
   }
@@ -766,7 +763,7 @@ fllf_status fllf_apply(fllf_plan p, const fllf_apply_args* a, float* d_out, size
   if (p && p->band)
     return fail(FLLF_ERR_INVALID_ARGUMENT,
                 "apply: row-band plans need the per-level calls (halo exchange between levels)");
-  return apply_impl(p, a, d_out, out_pitch_bytes, s, -1);
+  return apply_impl(p, a, d_out, out_pitch_bytes, s, 0, p ? p->nlev - 2 : 0);
 }
 
 fllf_status fllf_apply_accumulate(fllf_plan p, const fllf_apply_args* a, float* d_out, size_t out_pitch_bytes,
@@ -774,7 +771,7 @@ fllf_status fllf_apply_accumulate(fllf_plan p, const fllf_apply_args* a, float* 
   if (!p) return fail(FLLF_ERR_BAD_POINTER, "NULL plan");
   if (a && a->mode == FLLF_MAPS) return fail(FLLF_ERR_INVALID_ARGUMENT, "apply_accumulate: SCALAR / COEFFS only");
   if (p->band) return fail(FLLF_ERR_INVALID_ARGUMENT, "apply_accumulate: not for row-band plans");
-  return apply_impl(p, a, d_out, out_pitch_bytes, s, -1, true);
+  return apply_impl(p, a, d_out, out_pitch_bytes, s, 0, p->nlev - 2, true);
 }
 
 fllf_status fllf_ipc_alloc(size_t bytes, void** d_ptr, void* handle_out) {
@@ -819,8 +816,9 @@ fllf_status fllf_ipc_close(void* d_ptr) {
 
 fllf_status fllf_apply_level(fllf_plan p, const fllf_apply_args* a, float* d_out, size_t out_pitch_bytes, int level,
                              void* s) {
-  if (level < 0) return fail(FLLF_ERR_INVALID_ARGUMENT, "apply_level: level out of range");
-  return apply_impl(p, a, d_out, out_pitch_bytes, s, level);
+  if (!p) return fail(FLLF_ERR_BAD_POINTER, "NULL plan");
+  if (level < 0 || level >= p->nlev - 1) return fail(FLLF_ERR_INVALID_ARGUMENT, "apply_level: level out of range");
+  return apply_impl(p, a, d_out, out_pitch_bytes, s, level, level);
 }
 
 fllf_status fllf_plan_band_plane(fllf_plan p, int level, int kind, void** d_ptr, size_t* pitch_bytes, int* first_row,
@@ -848,25 +846,42 @@ fllf_status fllf_plan_band_plane(fllf_plan p, int level, int kind, void** d_ptr,
   return FLLF_OK;
 }
 
-// Design F is used for full-frame plans with levels >= 3 whose order count has
-// a supported per-warp split, unless FLLF_NO_FUSE=1.
-static bool fuse_enabled(fllf_plan p) {
+// Design F is used for the levels l >= 1 whose pixel count over the batch is
+// at least FLLF_FUSE_MIN_MP megapixels (default 4): from the finest level up to
+// the first smaller one ("fused levels" 1 .. LF-1); the coarser levels, where
+// a fused launch is latency-bound, keep design AB (build + apply).  Full-frame
+// plans with levels >= 3 whose order count has a supported per-warp split;
+// FLLF_NO_FUSE=1 disables it.  Returns LF (1 = design AB everywhere).
+static int fuse_levels(fllf_plan p) {
   static const bool off = [] {
     const char* e = std::getenv("FLLF_NO_FUSE");
     return e && e[0] == '1';
   }();
-  return !off && !p->band && p->nlev >= 3 && fllf::fuse_orders_per_warp(p->KL) > 0;
+  static const double min_mp = [] {
+    const char* e = std::getenv("FLLF_FUSE_MIN_MP");
+    return e ? std::atof(e) : 4.0;
+  }();
+  if (off || p->design == FLLF_DESIGN_AB || p->band || p->nlev < 3 || fllf::fuse_orders_per_warp(p->KL) <= 0)
+    return 1;
+  const int lmax = p->nlev - 1;
+  if (p->fused_levels > 0) return std::min(p->fused_levels + 1, lmax);
+  if (p->design == FLLF_DESIGN_F) return lmax;
+  int lf = 1;
+  while (lf < lmax && (double)p->d.batch * p->Hs[lf] * p->Ws[lf] >= min_mp * 1e6) ++lf;
+  return lf;
 }
 
-// Design F: build0; for l = 1 .. l_max-1 the fused
-// build step l -> l+1 + level-l order sum S_l (into D_l); the collapse
-// D_l += up(D_{l+1}) for l = l_max-2 .. 1; the level-0 apply (reads D_1).
-// All launches after the first are PDL-chained; each kernel waits for its
-// predecessor before it triggers the next one, so when a kernel starts every
-// kernel two or more places earlier has completed (the level-0 apply may
-// stage Z_1 before its own wait).
+// Design F, fused levels 1 .. LF-1: build0; for
+// l = 1 .. LF-1 the fused build step l -> l+1 + level-l order sum S_l (into
+// D_l); design AB for the coarser levels (build steps LF .. l_max-1, applies
+// l_max-1 .. LF, which leave the final D_LF); the collapse D_l += up(D_{l+1})
+// for l = min(LF, l_max-1)-1 .. 1 (D_{l_max-1} = S_{l_max-1} needs none); the
+// level-0 apply (reads D_1).  All launches after the first are PDL-chained;
+// each kernel waits for its predecessor before it triggers the next one, so
+// when a kernel starts every kernel two or more places earlier has completed
+// (the level-0 apply may stage Z_1 before its own wait).
 static fllf_status filter_fused(fllf_plan p, const float* d_img, size_t in_pitch_bytes, float* d_out,
-                                size_t out_pitch_bytes, void* s) {
+                                size_t out_pitch_bytes, void* s, int LF) {
   long long pitch;
   fllf_status st = check_image(d_img, in_pitch_bytes, p->d.W, "filter: d_img", &pitch);
   if (st != FLLF_OK) return st;
@@ -894,7 +909,7 @@ static fllf_status filter_fused(fllf_plan p, const float* d_img, size_t in_pitch
   fp.invT = (float)(1.0 / p->d.T);
   fp.dbg_lo = static_cast<const char*>(p->ws);
   fp.dbg_hi = fp.dbg_lo + p->ws_bytes;
-  for (int l = 1; l < lmax; ++l) {
+  for (int l = 1; l < LF; ++l) {
     fp.src = p->lv[l];
     fp.dst = p->lv[l + 1];
     fp.Hf = p->Hs[l];
@@ -909,7 +924,21 @@ static fllf_status filter_fused(fllf_plan p, const float* d_img, size_t in_pitch
     if (e != cudaSuccess) return cuda_fail(e, "fuse kernel launch");
     ++launches;
   }
-  for (int l = lmax - 2; l >= 1; --l) {
+  for (int l = LF; l < lmax; ++l) {  // design AB above the fused levels: build steps
+    st = build_level_impl(p, d_img, pitch, l, stream, pdl);
+    if (st != FLLF_OK) return st;
+    ++launches;
+  }
+  p->built = true;
+  p->img = d_img;
+  p->img_pitch = pitch;
+  if (LF < lmax) {  // ... and applies l_max-1 .. LF
+    st = apply_impl(p, nullptr, d_out, out_pitch_bytes, s, LF, lmax - 1, false, true);
+    if (st != FLLF_OK) return st;
+    launches += p->last_launches;
+    p->last_was_apply = false;
+  }
+  for (int l = std::min(LF, lmax - 1) - 1; l >= 1; --l) {
     fllf::CollapseParams cp{};
     const fllf::DevLevel& F = p->lv[l];
     const fllf::DevLevel& C = p->lv[l + 1];
@@ -933,10 +962,7 @@ static fllf_status filter_fused(fllf_plan p, const float* d_img, size_t in_pitch
     if (e != cudaSuccess) return cuda_fail(e, "collapse kernel launch");
     ++launches;
   }
-  p->built = true;
-  p->img = d_img;
-  p->img_pitch = pitch;
-  st = apply_impl(p, nullptr, d_out, out_pitch_bytes, s, 0, false, true);
+  st = apply_impl(p, nullptr, d_out, out_pitch_bytes, s, 0, 0, false, true);
   if (st != FLLF_OK) return st;
   p->last_launches = launches + 1;
   return FLLF_OK;
@@ -944,7 +970,8 @@ static fllf_status filter_fused(fllf_plan p, const float* d_img, size_t in_pitch
 
 static fllf_status filter_eager(fllf_plan p, const float* d_img, size_t in_pitch_bytes, float* d_out,
                                 size_t out_pitch_bytes, void* s) {
-  if (fuse_enabled(p)) return filter_fused(p, d_img, in_pitch_bytes, d_out, out_pitch_bytes, s);
+  const int lf = fuse_levels(p);
+  if (lf > 1) return filter_fused(p, d_img, in_pitch_bytes, d_out, out_pitch_bytes, s, lf);
   fllf_status st = fllf_build_fourier_pyramids(p, d_img, in_pitch_bytes, s);
   if (st != FLLF_OK) return st;
   const int nb = p->last_launches;
@@ -1026,8 +1053,11 @@ fllf_status fllf_filter_host(fllf_plan p, const float* h_img, float* h_out, void
   if (!h_img || !h_out) return fail(FLLF_ERR_BAD_POINTER, "filter_host: NULL host pointer");
   DeviceGuard guard(p->device);
   const size_t bytes = (size_t)p->d.batch * p->d.H * p->d.W * sizeof(float);
-  if (!p->stage_in) {
+  if (!p->stage_in || !p->stage_out) {
     if (cudaMalloc(&p->stage_in, bytes) != cudaSuccess || cudaMalloc(&p->stage_out, bytes) != cudaSuccess) {
+      if (p->stage_in) cudaFree(p->stage_in);
+      if (p->stage_out) cudaFree(p->stage_out);
+      p->stage_in = p->stage_out = nullptr;
       cudaGetLastError();
       return fail(FLLF_ERR_OUT_OF_MEMORY, "staging cudaMalloc failed");
     }
@@ -1042,11 +1072,36 @@ fllf_status fllf_filter_host(fllf_plan p, const float* h_img, float* h_out, void
   return FLLF_OK;
 }
 
+// Release everything pipe_setup created (any subset); leaves the plan as before setup.
+static void pipe_release(fllf_plan p) {
+  for (int i = 0; i < fllf_plan_s::kPipe; ++i) {
+    if (p->pipe_in[i]) cudaFree(p->pipe_in[i]);
+    if (p->pipe_out[i]) cudaFree(p->pipe_out[i]);
+    p->pipe_in[i] = p->pipe_out[i] = nullptr;
+    for (cudaEvent_t* ev : {&p->ev_in[i], &p->ev_done[i], &p->ev_out[i]}) {
+      if (*ev) cudaEventDestroy(*ev);
+      *ev = nullptr;
+    }
+  }
+  for (cudaEvent_t* ev : {&p->ev_pstart, &p->ev_pend}) {
+    if (*ev) cudaEventDestroy(*ev);
+    *ev = nullptr;
+  }
+  for (cudaStream_t* st : {&p->s_h2d, &p->s_d2h}) {
+    if (*st) cudaStreamDestroy(*st);
+    *st = nullptr;
+  }
+  cudaGetLastError();
+}
+
+// Staging buffers, copy streams and events of fllf_filter_host_frames, created
+// once; all or nothing (a failure releases what was created, so the next call
+// retries from scratch instead of running with missing pieces).
 static fllf_status pipe_setup(fllf_plan p, size_t bytes) {
-  if (p->pipe_in[0]) return FLLF_OK;
+  if (p->pipe_ready) return FLLF_OK;
   for (int i = 0; i < fllf_plan_s::kPipe; ++i) {
     if (cudaMalloc(&p->pipe_in[i], bytes) != cudaSuccess || cudaMalloc(&p->pipe_out[i], bytes) != cudaSuccess) {
-      cudaGetLastError();
+      pipe_release(p);
       return fail(FLLF_ERR_OUT_OF_MEMORY, "filter_host_frames: staging cudaMalloc failed");
     }
   }
@@ -1057,7 +1112,12 @@ static fllf_status pipe_setup(fllf_plan p, size_t bytes) {
   for (int i = 0; i < fllf_plan_s::kPipe; ++i)
     for (cudaEvent_t* ev : {&p->ev_in[i], &p->ev_done[i], &p->ev_out[i]})
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
-  return e == cudaSuccess ? FLLF_OK : cuda_fail(e, "filter_host_frames: stream / event creation");
+  if (e != cudaSuccess) {
+    pipe_release(p);
+    return cuda_fail(e, "filter_host_frames: stream / event creation");
+  }
+  p->pipe_ready = true;
+  return FLLF_OK;
 }
 
 fllf_status fllf_filter_host_frames(fllf_plan p, const float* h_in, size_t in_stride_bytes, float* h_out,
@@ -1316,6 +1376,13 @@ fllf_status fllf_naive_llf(fllf_plan p, const float* d_img, size_t pitch_bytes, 
   return FLLF_OK;
 }
 
+fllf_status fllf_plan_get_desc(fllf_plan p, fllf_plan_desc* out) {
+  if (!p || !out) return fail(FLLF_ERR_BAD_POINTER, "plan_get_desc: NULL argument");
+  *out = p->d;
+  out->device = p->device;
+  return FLLF_OK;
+}
+
 fllf_status fllf_plan_level_dims(fllf_plan p, int level, int* H, int* W) {
   if (!p || !H || !W) return fail(FLLF_ERR_BAD_POINTER, "NULL argument");
   if (level < 0 || level >= p->nlev) return fail(FLLF_ERR_INVALID_ARGUMENT, "level out of range");
@@ -1364,6 +1431,34 @@ fllf_status fllf_plan_set_profiling(fllf_plan p, int enable) {
   if (!p) return fail(FLLF_ERR_BAD_POINTER, "NULL plan");
   p->profiling = enable != 0;
   p->nrec = 0;
+  return FLLF_OK;
+}
+
+static void drop_graphs(fllf_plan p) {  // cached graphs hold the previous launch sequence
+  DeviceGuard guard(p->device);
+  for (auto& g : p->graphs)
+    if (g.exec) {
+      cudaGraphExecDestroy(g.exec);
+      g.exec = nullptr;
+    }
+}
+
+fllf_status fllf_plan_set_design(fllf_plan p, int design) {
+  if (!p) return fail(FLLF_ERR_BAD_POINTER, "NULL plan");
+  if (design != FLLF_DESIGN_AUTO && design != FLLF_DESIGN_AB && design != FLLF_DESIGN_F)
+    return fail(FLLF_ERR_INVALID_ARGUMENT, "set_design: FLLF_DESIGN_AUTO, _AB or _F");
+  drop_graphs(p);
+  p->design = design;
+  p->fused_levels = 0;
+  return FLLF_OK;
+}
+
+fllf_status fllf_plan_set_fused_levels(fllf_plan p, int n) {
+  if (!p) return fail(FLLF_ERR_BAD_POINTER, "NULL plan");
+  if (n < 0) return fail(FLLF_ERR_INVALID_ARGUMENT, "set_fused_levels: n >= 0");
+  drop_graphs(p);
+  p->fused_levels = n;
+  if (n == 0) p->design = FLLF_DESIGN_AUTO;
   return FLLF_OK;
 }
 

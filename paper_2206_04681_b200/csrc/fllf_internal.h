@@ -127,6 +127,7 @@ struct FuseParams {
   int Hf, Wf, Hc, Wc;  // dims of levels l and l+1
   int KL, kbase;       // local orders, global order of local order 0
   int rows_per_strip;  // coarse rows per CTA
+  int exp;             // A/B experiments (FLLF_FUSE_EXP; 0 in production)
   float invT;          // 1/T
   // Clenshaw coefficient pairs per local order, as ApplyParams::cw
   float2 cw[FLLF_MAX_K][4];

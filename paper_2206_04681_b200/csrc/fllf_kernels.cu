@@ -1173,7 +1173,8 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0, MAPS>()) k_apply_cl
       unsigned char* hdr = smem + HOFF + hb * HB;
       if (nt >= 2) mbar_wait_parity(&hempty[hb], ((nt >> 1) & 1) ^ 1u);
       // interior tiles: the 8 fine g rows / 6 coarse D rows are contiguous -> one tensor copy each
-      const bool tmg = P.use_tm_g && 2 * T.r0 + 7 <= min(P.Hf - 1, P.fr_hi);
+      // (only when the consumers take g from the header: tma_g; else they load it themselves)
+      const bool tmg = tma_g && P.use_tm_g && 2 * T.r0 + 7 <= min(P.Hf - 1, P.fr_hi);
       if (tmg) {
         if (elect_one()) {
           mbar_arrive_expect_tx(&gfull[hb], 8 * HDR_G_ROW);

@@ -88,6 +88,9 @@ _SIGS = {
     "fllf_plan_last_launch_count": (ctypes.c_int, [_P]),
     "fllf_plan_set_profiling": (ctypes.c_int, [_P, ctypes.c_int]),
     "fllf_plan_set_graphs": (ctypes.c_int, [_P, ctypes.c_int]),
+    "fllf_plan_set_design": (ctypes.c_int, [_P, ctypes.c_int]),
+    "fllf_plan_set_fused_levels": (ctypes.c_int, [_P, ctypes.c_int]),
+    "fllf_plan_get_desc": (ctypes.c_int, [_P, ctypes.POINTER(fllf_plan_desc)]),
     "fllf_plan_kernel_times": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
                                               ctypes.POINTER(ctypes.c_int),
                                               ctypes.POINTER(ctypes.c_float),
@@ -342,9 +345,13 @@ def fllf_filter(plan, img, out, stream=None) -> None:
 
 def fllf_filter_host(plan, h_img, h_out, stream=None) -> None:
     """h_img / h_out: contiguous float32 CPU tensors (pin them for async copies)."""
+    import torch
+    d = fllf_plan_get_desc(plan)
     for t, n in ((h_img, "h_img"), (h_out, "h_out")):
         if t.is_cuda or not t.is_contiguous():
             raise TypeError(f"{n} must be a contiguous host tensor")
+        if t.dtype != torch.float32 or t.numel() < d["batch"] * d["H"] * d["W"]:
+            raise ValueError(f"{n} must be float32 with batch*H*W elements")
     _check(lib.fllf_filter_host(plan, h_img.data_ptr(), h_out.data_ptr(), _stream_handle(stream)))
 
 
@@ -355,9 +362,14 @@ def fllf_filter_host_frames(plan, h_in, in_stride_bytes, h_out, out_stride_bytes
     for t, n in ((h_in, "h_in"), (h_out, "h_out")):
         if t.is_cuda or not t.is_contiguous():
             raise TypeError(f"{n} must be a contiguous host tensor")
+    import torch
+    d = fllf_plan_get_desc(plan)
+    batch_bytes = d["batch"] * d["H"] * d["W"] * 4
     for t, st, n in ((h_in, in_stride_bytes, "h_in"), (h_out, out_stride_bytes, "h_out")):
-        if nframes > 0 and (nframes - 1) * st + 1 > t.numel() * 4:
-            raise ValueError(f"{n} too small for {nframes} batches at stride {st}")
+        if t.dtype != torch.float32:
+            raise TypeError(f"{n} must be float32")
+        if nframes > 0 and (nframes - 1) * st + batch_bytes > t.numel() * t.element_size():
+            raise ValueError(f"{n} too small for {nframes} batches of {batch_bytes} bytes at stride {st}")
     _check(lib.fllf_filter_host_frames(plan, h_in.data_ptr(), int(in_stride_bytes), h_out.data_ptr(),
                                        int(out_stride_bytes), int(nframes), _stream_handle(stream)))
 
@@ -467,6 +479,26 @@ def fllf_plan_set_graphs(plan, enable: bool) -> None:
     _check(lib.fllf_plan_set_graphs(plan, 1 if enable else 0))
 
 
+FLLF_DESIGN_AUTO, FLLF_DESIGN_AB, FLLF_DESIGN_F = 0, 1, 2
+
+
+def fllf_plan_set_design(plan, design: int) -> None:
+    """Design of fllf_filter: FLLF_DESIGN_AUTO (default), FLLF_DESIGN_AB or FLLF_DESIGN_F."""
+    _check(lib.fllf_plan_set_design(plan, int(design)))
+
+
+def fllf_plan_set_fused_levels(plan, n: int) -> None:
+    """Design F on levels 1..n, AB above (0: FLLF_DESIGN_AUTO)."""
+    _check(lib.fllf_plan_set_fused_levels(plan, int(n)))
+
+
+def fllf_plan_get_desc(plan) -> dict:
+    """The plan's effective description (fllf_plan_desc fields)."""
+    d = fllf_plan_desc()
+    _check(lib.fllf_plan_get_desc(plan, ctypes.byref(d)))
+    return {name: getattr(d, name) for name, _ in fllf_plan_desc._fields_}
+
+
 def fllf_plan_kernel_times(plan, capacity: int = 64):
     """[(kind name, level, milliseconds)] for the launches of the last build(+apply)."""
     kind = (ctypes.c_int * capacity)()
@@ -496,19 +528,46 @@ class Plan:
     row_begin: int = 0
     row_end: int = 0
 
+    design: int = FLLF_DESIGN_AUTO
+
     def __post_init__(self):
         self.handle = fllf_plan_create_ex(self.H, self.W, self.levels, self.K, self.T, self.sigma_r,
                                           self.m, self.batch, self.k_begin, self.k_end,
                                           self.include_base, self.device, self.row_begin, self.row_end)
+        self._dev = fllf_plan_get_desc(self.handle)["device"]
+        if self.design != FLLF_DESIGN_AUTO:
+            fllf_plan_set_design(self.handle, self.design)
+
+    def _check_frames(self, t, name: str) -> None:
+        """A full-frame plan's image / output: (H, W) or (batch, H, W) on the plan's device."""
+        if self.row_begin or self.row_end:
+            return  # band plans take the band's rows (see fllf_plan_desc)
+        if not hasattr(t, "shape") or tuple(t.shape[-2:]) != (self.H, self.W):
+            raise ValueError(f"{name} must end in ({self.H}, {self.W}), got {tuple(getattr(t, 'shape', ()))}")
+        frames = 1
+        for n in t.shape[:-2]:
+            frames *= int(n)
+        if frames != self.batch:
+            raise ValueError(f"{name} holds {frames} frames, the plan's batch is {self.batch}")
+        if getattr(t, "is_cuda", False) and t.device.index != self._dev:
+            raise ValueError(f"{name} is on cuda:{t.device.index}, the plan on cuda:{self._dev}")
 
     def build(self, img, stream=None):
+        self._check_frames(img, "img")
         fllf_build_fourier_pyramids(self.handle, img, stream)
 
     def apply(self, out, **kw):
+        self._check_frames(out, "out")
         fllf_apply(self.handle, out, **kw)
 
     def filter(self, img, out, stream=None):
+        self._check_frames(img, "img")
+        self._check_frames(out, "out")
         fllf_filter(self.handle, img, out, stream)
+
+    def set_design(self, design: int) -> None:
+        fllf_plan_set_design(self.handle, design)
+        self.design = design
 
     def level_dims(self, level):
         return fllf_plan_level_dims(self.handle, level)

@@ -42,7 +42,7 @@ def run_both(F, x, levels, K, T, sig, m, pad=0, **kw):
         d_in = torch.from_numpy(x).cuda()
     o_f = torch.full((B, H, W), float("nan"), device="cuda")
     o_ab = torch.full((B, H, W), float("nan"), device="cuda")
-    with F.Plan(H, W, levels, K, T, sig, m, batch=B, **kw) as p:
+    with F.Plan(H, W, levels, K, T, sig, m, batch=B, design=F.FLLF_DESIGN_F, **kw) as p:
         p.filter(d_in, o_f)
         launches = p.launches
         p.build(d_in)
@@ -90,7 +90,7 @@ def test_fused_pyramids_identical(F):
     d_in = torch.from_numpy(img).cuda()
     out = torch.empty_like(d_in)
     planes = {}
-    with F.Plan(H, W, levels, K, 510.0, 30.0, 3.0) as p:
+    with F.Plan(H, W, levels, K, 510.0, 30.0, 3.0, design=F.FLLF_DESIGN_F) as p:
         for tag in ("F", "AB"):
             if tag == "F":
                 p.filter(d_in, out)
@@ -117,7 +117,7 @@ def test_fused_then_reapply(F):
     r2 = O.fourier_llf(img.astype(np.float64), levels, K, 510.0, a=a2)
     d_in = torch.from_numpy(img).cuda()
     o = torch.empty_like(d_in)
-    with F.Plan(H, W, levels, K, 510.0, 30.0, 2.0) as p:
+    with F.Plan(H, W, levels, K, 510.0, 30.0, 2.0, design=F.FLLF_DESIGN_F) as p:
         p.filter(d_in, o)
         torch.cuda.synchronize()
         assert maxerr(o.cpu().numpy(), r1) <= TOL_OUT
@@ -158,3 +158,39 @@ def test_band_plans_reject_whole_pass_calls(F):
             with pytest.raises(F.FllfError) as e:
                 call()
             assert e.value.status == F.FLLF_ERR_INVALID_ARGUMENT
+
+
+@pytest.mark.parametrize("n", [1, 2, 3])
+def test_mixed_fused_and_ab_levels(F, n):
+    """Design F on levels 1..n and AB above (what FLLF_DESIGN_AUTO picks when
+    only the fine levels are large): the sequence build0, fused 1..n, build /
+    apply n+1.., collapse n..1, apply0 matches the oracle and pure AB."""
+    H, W, levels, K = 150, 201, 6, 8
+    img = synth.uniform_image(H, W, seed=615)
+    ref = O.fourier_llf(img.astype(np.float64), levels, K, 510.0, 30.0, 3.0)
+    d_in = torch.from_numpy(img).cuda()
+    o_f = torch.full_like(d_in, float("nan"))
+    o_ab = torch.full_like(d_in, float("nan"))
+    with F.Plan(H, W, levels, K, 510.0, 30.0, 3.0) as p:
+        F.fllf_plan_set_fused_levels(p.handle, n)
+        p.filter(d_in, o_f)
+        lmax = levels - 1
+        assert p.launches == 1 + n + 2 * (lmax - 1 - n) + (min(n + 1, lmax - 1) - 1) + 1, p.launches
+        p.set_design(F.FLLF_DESIGN_AB)
+        p.filter(d_in, o_ab)
+        assert p.launches == 2 * lmax
+        torch.cuda.synchronize()
+    assert maxerr(o_f.cpu().numpy(), ref) <= TOL_OUT
+    assert maxerr(o_f.cpu().numpy(), o_ab.cpu().numpy()) <= TOL_AB
+
+
+def test_design_api_errors(F):
+    with F.Plan(64, 64, 3, 4) as p:
+        with pytest.raises(F.FllfError):
+            F.fllf_plan_set_design(p.handle, 7)
+        with pytest.raises(F.FllfError):
+            F.fllf_plan_set_fused_levels(p.handle, -1)
+        d = F.fllf_plan_get_desc(p.handle)
+        assert (d["H"], d["W"], d["levels"], d["K"], d["batch"], d["k_begin"], d["k_end"]) == (64, 64, 3, 4, 1, 1, 5)
+        with pytest.raises(ValueError):   # shape checks of the binding
+            p.filter(torch.zeros((64, 60), device="cuda"), torch.zeros((64, 64), device="cuda"))
