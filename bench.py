@@ -2,16 +2,18 @@
 """Fourier LLF throughput on B200 -- the driver's bench contract.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fllf|reference]
-                    [--workload config2|config5]
+                    [--workload config5|config2|config3|config4|bands|color]
 
 One step = one pass of the whole hot path (build the 2K+1 pyramids, product-sum,
 collapse) over one batch of synthetic input already resident in HBM.  Default
-workload: BASELINE.json configs[1] (1080x1920 grayscale, 6 levels, K=8,
-T=510, sigma_r=30, m=3), one frame per rank per step; with N ranks each rank
-filters its own frame (frame data-parallel, no collective: "scaling": "weak").
-L2 (126 MB) is flushed between timed steps (a 2x-L2 buffer write, outside the
-per-step events); step durations are CUDA events on the launch stream, summed
-over the K steps, max over ranks.  Rank 0 prints ONE JSON line.
+workload: BASELINE.json configs[4] (64 frames 1080x1920 grayscale, 6 levels,
+K=16, T=510, sigma_r=30, m=3), the configuration the north star partitions
+("frames split data-parallel over 8 GPUs"): with N ranks each rank filters
+64/N of the frames (no collective; "scaling": "strong" -- the same 64 frames
+at every N).  `--workload config2` is the single-frame configs[1].  L2
+(126 MB) is flushed between timed steps (a 2x-L2 buffer write, outside the
+per-step events); step durations are CUDA events on the launch stream,
+summed over the K steps, max over ranks.  Rank 0 prints ONE JSON line.
 See DESIGN.md "Measurement" for every key.
 """
 from __future__ import annotations
@@ -153,48 +155,86 @@ def algorithmic_bytes(kind, level, dims, K, frames, levels):
 
 
 # ------------------------------------------------------------ CPU baseline
-def cpu_baseline(img, c, budget_s=12.0, max_frames=6):
-    """The oracle as it stands (numpy fp64), on full frames of the workload."""
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def _oracle_job(job):
+    """One oracle run in a worker process (single-threaded numpy fp64):
+    (image, levels, K, T, sigma_r, m) -> seconds."""
+    img, levels, K, T, sig, m = job
     from oracle import fllf_oracle as O
-    n, t0 = 0, time.perf_counter()
-    while n < max_frames:
-        O.fourier_llf(img.astype(np.float64), c["levels"], c["K"], c["T"], c["sigma_r"], c["m"])
-        n += 1
-        if time.perf_counter() - t0 > budget_s:
-            break
-    dt = time.perf_counter() - t0
-    H, W = img.shape
-    return {"value": round(n * H * W / 1e6 / dt, 4), "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{n} full {H}x{W} frame(s) of the workload through oracle/fllf_oracle.py "
-                      f"(numpy fp64, single-threaded), {dt:.1f} s"}
+    t0 = time.perf_counter()
+    O.fourier_llf(img.astype(np.float64), levels, K, T, sig, m)
+    return time.perf_counter() - t0
+
+
+def _pool(n):
+    """A process pool of n single-threaded workers (spawned: no CUDA state)."""
+    import multiprocessing as mp
+    for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ.setdefault(v, "1")
+    return mp.get_context("spawn").Pool(n)
+
+
+def cpu_baseline(frames, c):
+    """The oracle as it stands (numpy fp64) on full frames of the workload,
+    timed on the host: all cores (one frame per worker process, `cores` frames
+    at once) and one core (one frame), BASELINE.md section 3."""
+    cores = host_cores()
+    H, W = frames.shape[-2:]
+    args = (c["levels"], c["K"], c["T"], c["sigma_r"], c["m"])
+    jobs = [(frames[i % len(frames)], *args) for i in range(cores)]
+    with _pool(cores) as pool:
+        pool.map(_oracle_job, [(frames[0][:64, :64], *args)] * cores)  # start-up, imports
+        t0 = time.perf_counter()
+        pool.map(_oracle_job, jobs)
+        dt_all = time.perf_counter() - t0
+    dt_one = _oracle_job((frames[0], *args))
+    mp_all = cores * H * W / 1e6 / dt_all
+    mp_one = H * W / 1e6 / dt_one
+    return {"value": round(mp_all, 4), "unit": UNIT, "cores": cores, "kind": "oracle",
+            "value_1_core": round(mp_one, 4),
+            "sample": f"{cores} full {H}x{W} frame(s) of the workload through oracle/fllf_oracle.py "
+                      f"(numpy fp64), one per worker process on {cores} host cores, {dt_all:.1f} s; "
+                      f"1 core: 1 frame, {dt_one:.1f} s"}
 
 
 # --------------------------------------------------------------- reference
 def run_reference(args):
-    """--impl reference: the oracle timed on host cores on a bounded sample of
-    the same workload (a 270x480 crop = 1/16 of a config-2 frame per step)."""
+    """--impl reference: the oracle timed on the host's cores on a bounded
+    sample of the same workload: per step, one 270x480 crop (1/16 of a
+    1080x1920 frame) per core, the crops in parallel worker processes."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    from oracle import fllf_oracle as O
     from paper_2206_04681_b200 import synth
     wl = WORKLOADS[args.workload]
     c = synth.CONFIGS[wl["cfg"]]
-    img = synth.config2_image(seed=2000 if wl["cfg"] == 2 else 5000)[:270, :480].astype(np.float64)
-    for _ in range(args.warmup):
-        O.fourier_llf(img, c["levels"], c["K"], c["T"], c["sigma_r"], c["m"])
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        O.fourier_llf(img, c["levels"], c["K"], c["T"], c["sigma_r"], c["m"])
-    dt = time.perf_counter() - t0
-    v = args.steps * img.size / 1e6 / dt
-    sample = f"270x480 crop (1/16 of a 1080x1920 frame) of the {args.workload} workload per step"
+    base = synth.config2_image(seed=2000 if wl["cfg"] == 2 else 5000)
+    cores = host_cores()
+    crops = [base[(i // 4 % 4) * 270:(i // 4 % 4 + 1) * 270, (i % 4) * 480:(i % 4 + 1) * 480] for i in range(cores)]
+    jobs = [(cr, c["levels"], c["K"], c["T"], c["sigma_r"], c["m"]) for cr in crops]
+    with _pool(cores) as pool:
+        for _ in range(args.warmup):
+            pool.map(_oracle_job, jobs)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            pool.map(_oracle_job, jobs)
+        dt = time.perf_counter() - t0
+    px = args.steps * cores * 270 * 480
+    v = px / 1e6 / dt
+    sample = (f"per step {cores} 270x480 crops (1/16 of a 1080x1920 frame each) of the {args.workload} "
+              f"workload, one per worker process on {cores} host cores")
     line = {"metric": METRIC, "value": round(v, 4), "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * dt / args.steps, 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
             "config": {"workload": wl["desc"], "sample": sample},
-            "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": 1, "kind": "oracle",
+            "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": round(v, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -418,7 +458,8 @@ def run_sharded(args, c, wl, world, rank, local):
     rgb = synth.config3_rgb()
     img = torch.from_numpy(rgb).cuda()
     out = torch.empty_like(img)
-    if args.combine == "p2p":
+    combine = args.combine if args.combine != "auto" else ("p2p" if world > 1 else "nccl")
+    if combine == "p2p":
         comb = D.P2PCombine(img, levels, K, c["T"], c["sigma_r"], c["m"])
         fn = None
 
@@ -491,12 +532,13 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["fllf", "reference"], default="fllf")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="config2")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="config5")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--combine", choices=["nccl", "p2p"], default="nccl",
+    ap.add_argument("--combine", choices=["auto", "nccl", "p2p"], default="auto",
                     help="config3: NCCL reduce per channel, or the fused combine "
-                         "(fllf_apply_accumulate into the owner's CUDA-IPC-mapped output)")
+                         "(fllf_apply_accumulate into the owner's CUDA-IPC-mapped output); "
+                         "auto = p2p with more than one rank, nccl with one")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -668,7 +710,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(imgs[0], c)
+        cpu = cpu_baseline(imgs, c)
     clk.close()
     plan.close()
     if rank == 0:

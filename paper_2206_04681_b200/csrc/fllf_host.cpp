@@ -13,6 +13,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: no-ops unless a tool (nsys) is attached
+
 #include "fllf.h"
 #include "fllf_internal.h"
 
@@ -177,12 +179,45 @@ bool encode_real_map(CUtensorMap* m, const float* base, int W, int H, int planes
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Bracket one launch with profiling events (no-op when profiling is off).
+// NVTX range around each kernel launch ("fllf <kind>", payload = level), so
+// an nsys trace shows every libfllf launch beside the NCCL / copy activity.
+struct NvtxRange {
+  NvtxRange(const char* name, int level) {
+    nvtxEventAttributes_t a = {};
+    a.version = NVTX_VERSION;
+    a.size = NVTX_EVENT_ATTRIB_STRUCT_SIZE;
+    a.messageType = NVTX_MESSAGE_TYPE_ASCII;
+    a.message.ascii = name;
+    a.payloadType = NVTX_PAYLOAD_TYPE_INT32;
+    a.payload.iValue = level;
+    nvtxRangePushEx(&a);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
+const char* kind_name(int kind) {
+  switch (kind) {
+    case FLLF_K_BUILD0: return "fllf build0";
+    case FLLF_K_BUILD: return "fllf build";
+    case FLLF_K_MAPBUILD: return "fllf mapbuild";
+    case FLLF_K_APPLY: return "fllf apply";
+    case FLLF_K_APPLY0: return "fllf apply0";
+    case FLLF_K_FUSE: return "fllf fuse";
+    case FLLF_K_COLLAPSE: return "fllf collapse";
+  }
+  return "fllf";
+}
+
+// Bracket one launch with profiling events (no-op when profiling is off) and
+// an NVTX range.
 struct ProfScope {
   fllf_plan p;
   cudaStream_t s;
   int idx = -1;
-  ProfScope(fllf_plan p_, cudaStream_t s_, int kind, int level) : p(p_), s(s_) {
+  NvtxRange range;
+  ProfScope(fllf_plan p_, cudaStream_t s_, int kind, int level) : p(p_), s(s_), range(kind_name(kind), level) {
     if (!p->profiling) return;
     idx = p->nrec++;
     if ((int)p->ev_start.size() <= idx) {
@@ -1209,6 +1244,7 @@ fllf_status fllf_rgb_to_yuv(const float* d_rgb, float* d_yuv, int H, int W, size
   long long pitch;
   fllf_status st = color_common(d_rgb, d_yuv, H, W, pitch_bytes, &pitch);
   if (st != FLLF_OK) return st;
+  NvtxRange r("fllf rgb_to_yuv", 0);
   cudaError_t e = fllf::launch_rgb_to_yuv(color_params(d_rgb, d_yuv, H, W, pitch), static_cast<cudaStream_t>(s));
   return e == cudaSuccess ? FLLF_OK : cuda_fail(e, "rgb_to_yuv launch");
 }
@@ -1217,6 +1253,7 @@ fllf_status fllf_yuv_to_rgb(const float* d_yuv, float* d_rgb, int H, int W, size
   long long pitch;
   fllf_status st = color_common(d_yuv, d_rgb, H, W, pitch_bytes, &pitch);
   if (st != FLLF_OK) return st;
+  NvtxRange r("fllf yuv_to_rgb", 0);
   cudaError_t e = fllf::launch_yuv_to_rgb(color_params(d_yuv, d_rgb, H, W, pitch), static_cast<cudaStream_t>(s));
   return e == cudaSuccess ? FLLF_OK : cuda_fail(e, "yuv_to_rgb launch");
 }
@@ -1251,6 +1288,7 @@ fllf_status fllf_gain_map(const float* d_y, size_t y_pitch_bytes, int H, int W, 
   gp.m_lo = g->m_lo;
   gp.m_hi = g->m_hi;
   gp.inv_vref = 1.0 / g->v_ref;
+  NvtxRange r("fllf gain_map", 0);
   cudaError_t e = fllf::launch_gain_map(gp, static_cast<cudaStream_t>(s));
   return e == cudaSuccess ? FLLF_OK : cuda_fail(e, "gain_map launch");
 }
@@ -1360,6 +1398,7 @@ fllf_status fllf_naive_llf(fllf_plan p, const float* d_img, size_t pitch_bytes, 
   const int lmax = p->nlev - 1;
   for (int l = 0; l < lmax; ++l) {
     np.level = l;
+    NvtxRange r("fllf naive_level", l);
     cudaError_t e = fllf::launch_naive_level(np, stream);
     if (e != cudaSuccess) return cuda_fail(e, "naive level launch");
   }

@@ -26,6 +26,29 @@ from dataclasses import dataclass
 from typing import Callable, List
 
 
+class _nvtx:
+    """NVTX range (torch.cuda.nvtx) when CUDA is present; a no-op on CPU-only hosts."""
+
+    def __init__(self, msg: str):
+        self.msg = msg
+        self.on = False
+
+    def __enter__(self):
+        try:
+            import torch
+            if torch.cuda.is_available():
+                torch.cuda.nvtx.range_push(self.msg)
+                self.on = True
+        except Exception:  # pragma: no cover
+            pass
+        return self
+
+    def __exit__(self, *exc):
+        if self.on:
+            import torch
+            torch.cuda.nvtx.range_pop()
+
+
 def frame_partition(n_frames: int, world: int, rank: int) -> tuple[int, int]:
     """(first frame, count) of rank's contiguous, balanced slice."""
     base, extra = divmod(n_frames, world)
@@ -97,17 +120,28 @@ def sharded_filter(partial_fn: Callable, out, channels: int, K: int, group=None,
     mine = order_partition(channels, K, world)[rank]
     if batch_channels:
         runs = channel_runs(mine)
-        done = set()
+        owned = {c for r in runs for c in range(r.channel, r.channel + r.nch)}
         works = []
+        nxt = 0  # next channel to reduce: every rank issues the reduces in channel order
+
+        def reduce_upto(last):
+            nonlocal nxt
+            while nxt <= last:
+                if nxt not in owned:
+                    out[nxt].zero_()
+                with _nvtx(f"fllf reduce channel {nxt}"):
+                    w = dist.reduce(out[nxt], dst=dst, op=dist.ReduceOp.SUM, group=group, async_op=overlap)
+                if overlap:
+                    works.append(w)
+                nxt += 1
+
         for r in runs:
-            partial_fn(r, out[r.channel:r.channel + r.nch])
-            done.update(range(r.channel, r.channel + r.nch))
-        for c in range(channels):
-            if c not in done:
-                out[c].zero_()
-            w = dist.reduce(out[c], dst=dst, op=dist.ReduceOp.SUM, group=group, async_op=overlap)
-            if overlap:
-                works.append(w)
+            # the run's kernels are enqueued; its channels' reduces go out now, so
+            # they wait only for the work queued so far and overlap the next run
+            with _nvtx(f"fllf partial channels {r.channel}..{r.channel + r.nch - 1}"):
+                partial_fn(r, out[r.channel:r.channel + r.nch])
+            reduce_upto(r.channel + r.nch - 1)
+        reduce_upto(channels - 1)
         for w in works:
             w.wait()
         return works
@@ -350,9 +384,10 @@ def band_filter(gb: GpuBand, img_band, out_band, group=None):
     iptr = img_band.data_ptr() + top_in * ipitch
     for step in band_schedule(gb.levels):
         if step[0] == "xchg":
-            for kind in step[2]:
-                v, first = gb.view(step[1], kind)
-                exchange_halos(v, first, gb.own(step[1]), group, up, down)
+            with _nvtx(f"fllf halo exchange level {step[1]}"):
+                for kind in step[2]:
+                    v, first = gb.view(step[1], kind)
+                    exchange_halos(v, first, gb.own(step[1]), group, up, down)
         else:
             gb.run_step(step, iptr, ipitch, out_band.data_ptr(), out_band.stride(0) * 4)
 

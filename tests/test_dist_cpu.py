@@ -81,8 +81,14 @@ def _worker(rank, world, port, img, args, result_path):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [1, 2])
-def test_sharded_filter_gloo_equals_full(tmp_path, world):
+@pytest.mark.parametrize("world,batch", [(1, True), (2, False), (2, True), (3, True)])
+def test_sharded_filter_gloo_equals_full(tmp_path, monkeypatch, world, batch):
+    """Order sharding with one reduce per channel.  batch: consecutive channels
+    with one order range run as one batched call, and each run's reduces are
+    issued right after it (every rank in channel order, zero-filled channels
+    without units included) -- world 3 gives ranks owning different channel
+    sets, so a rank-dependent reduce order would hang or mix channels."""
+    monkeypatch.setenv("FLLF_TEST_BATCH_CH", "1" if batch else "0")
     rng = np.random.default_rng(3)
     img = rng.uniform(0, 255, (3, 24, 21))
     args = (3, 5, 510.0, 20.0, 2.0)
