@@ -63,8 +63,11 @@ constexpr int FUSE_BAR = 1;    // named barrier id of the batch hand-over
 // warps per CTA (one per NC-order chunk), bounded so that the CTA fits one
 // SM's register file at 128 registers per thread (16 warps = 4 per SMSP)
 constexpr int FUSE_MAX_WARPS = 16;
-// order-sum batch: NB fine row pairs = NB x 128 pixels, one per lane of the CTA
-__host__ __device__ inline int fuse_nb(int nw) { return nw >= 8 ? nw / 4 : 1; }
+// order-sum batch: NB = 3 fine row pairs (384 pixels), the steps of one
+// iteration of the stream loop (unrolled by 3 for the register rotation), so
+// the order sums sit at one place in the loop
+constexpr int FUSE_NB = 3;
+__host__ __device__ inline int fuse_nb(int) { return FUSE_NB; }
 
 __device__ __forceinline__ void bar_sync_id(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -118,64 +121,6 @@ struct FuseLayout {
   }
   __host__ __device__ static int smem(int KL) { return ring_off(KL, KL / NC); }
 };
-
-// Order sums (Eq. 14) of one batch of cnt fine row pairs (rows from row0):
-//   S = sum_k a_k Im(e^{-i k theta} V_k) = sum_k (c_cos,k cos k theta + c_sin,k sin k theta),
-// theta = w_1 g, from the coefficient pairs c_k in C and g in Gb, by
-// Clenshaw's recurrence (descending k: b_k = c_k + 2 cos theta b_{k+1} - b_{k+2};
-// see k_apply_cl), stored into D_l.  Pixel p = tid + j * nthreads of the
-// batch (pair q = p / 128, row r, fine column f).  Out of line: it runs once
-// per batch, and keeping it out of the unrolled stream loop keeps the hot
-// code in the instruction cache.
-__device__ __noinline__ void fuse_order_sum(const FuseParams& P, uint32_t sbase, int goff, float* dbase, int row0,
-                                            int cnt, int cb) {
-  const int KL = P.KL;
-  const int nthreads = blockDim.x;
-  const long long pitch = P.src.pitch;
-  const int Hf = P.Hf;
-#pragma unroll 1
-  for (int p = threadIdx.x; p < cnt * 128; p += nthreads) {
-    const int q = p >> 7, r = (p >> 6) & 1, f = p & 63;
-    const float g = lds1(sbase + goff + ((q * 2 + r) * 64 + f) * 4);
-    float sn, c1;
-    sincos_turns(g, P.invT, &sn, &c1);
-    const float2 tc = bc(2.f * c1);
-    float2 b1 = make_float2(0.f, 0.f), b2 = b1;
-    uint32_t a = sbase + ((q * KL + KL - 1) * 2 + r) * 512 + f * 8;
-    int k = KL;
-#pragma unroll 1
-    for (; k >= 4; k -= 4, a -= 4096) {
-      const float2 c3 = lds2(a), c2 = lds2(a - 1024), c1v = lds2(a - 2048), c0 = lds2(a - 3072);
-      b2 = pfma(tc, b1, padd(c3, pneg(b2)));
-      b1 = pfma(tc, b2, padd(c2, pneg(b1)));
-      b2 = pfma(tc, b1, padd(c1v, pneg(b2)));
-      b1 = pfma(tc, b2, padd(c0, pneg(b1)));
-    }
-#pragma unroll 1
-    for (; k > 0; --k, a -= 1024) {
-      const float2 nb2 = pfma(tc, b1, padd(lds2(a), pneg(b2)));
-      b2 = b1;
-      b1 = nb2;
-    }
-    // b1 = b_{k0}, b2 = b_{k0+1}
-    float res;
-    if (P.kbase == 1) {
-      res = fmaf(b1.x, c1, fmaf(b1.y, sn, -b2.x));
-    } else {
-      float sk, ck;
-      sincos_turns_n(g, P.invT, P.kbase, &sk, &ck);
-      const float cm = fmaf(ck, c1, sk * sn), sm = fmaf(sk, c1, -ck * sn);  // e^{i (k0-1) theta}
-      res = fmaf(b1.x, ck, fmaf(b1.y, sk, -fmaf(b2.x, cm, b2.y * sm)));
-    }
-    const int row = row0 + 2 * q + r;
-    const int col = 2 * (FUSE_COLS * cb - 2) + f;  // lanes 2..29 own f in [4, 60)
-    if (f >= 4 && f < 60 && col < P.Wf && row < Hf) {
-      float* sp = dbase + (long long)row * pitch + col;
-      FLLF_DBG_STORE(P, sp, 4);
-      *sp = res;
-    }
-  }
-}
 
 // ---- one warp: NC orders of the strip (DO_G: warp 0 also builds G;
 // ROWS_IN: no fine row of the strip needs reflection)
@@ -381,12 +326,67 @@ struct FuseWarp {
       sts2(gb, lo2(gg));
       sts2(gb + 256, hi2(gg));
     }
-    if (++q == nb || n == R - 1) {
-      bar_sync_id(FUSE_BAR, nw * 32);  // the batch's C and g are complete
-      if (!(P.exp & 1)) fuse_order_sum(P, sbase_, L::g_off(P.KL), dbase, 2 * (o0 + n + 1 - q), q, cb_);
-      bar_sync_id(FUSE_BAR, nw * 32);  // ... and consumed
-      q = 0;
+    ++q;
+  }
+
+  // Order sums (Eq. 14) of the batch of cnt fine row pairs just completed
+  // (own pairs n0 .. n0+cnt-1): per pixel p = tid + j * 32 nw (pair q = p/128,
+  // row r, fine column f)
+  //   S = sum_k a_k Im(e^{-i k theta} V_k) = sum_k (c_cos,k cos k theta + c_sin,k sin k theta),
+  // theta = w_1 g, from the coefficient pairs c_k in C and g in Gb, by
+  // Clenshaw's recurrence (descending k: b_k = c_k + 2 cos theta b_{k+1} - b_{k+2};
+  // see k_apply_cl), stored into D_l.  Between two CTA barriers: C / Gb are
+  // complete before, consumed after.
+  __device__ __forceinline__ void order_sum(int n0, int cnt) {
+    bar_sync_id(FUSE_BAR, nw * 32);
+    if (!(P.exp & 1)) {
+      const int KL = P.KL;
+      const int goff = L::g_off(KL);
+      const int row0 = 2 * (o0 + n0);
+#pragma unroll 1
+      for (int p = warp * 32 + lane; p < cnt * 128; p += nw * 32) {
+        const int q = p >> 7, r = (p >> 6) & 1, f = p & 63;
+        const float g = lds1(sbase_ + goff + ((q * 2 + r) * 64 + f) * 4);
+        float sn, c1;
+        sincos_turns(g, P.invT, &sn, &c1);
+        const float2 tc = bc(2.f * c1);
+        float2 b1 = make_float2(0.f, 0.f), b2 = b1;
+        uint32_t a = sbase_ + ((q * KL + KL - 1) * 2 + r) * 512 + f * 8;
+        int k = KL;
+#pragma unroll 1
+        for (; k >= 4; k -= 4, a -= 4096) {
+          const float2 c3 = lds2(a), c2 = lds2(a - 1024), c1v = lds2(a - 2048), c0 = lds2(a - 3072);
+          b2 = pfma(tc, b1, padd(c3, pneg(b2)));
+          b1 = pfma(tc, b2, padd(c2, pneg(b1)));
+          b2 = pfma(tc, b1, padd(c1v, pneg(b2)));
+          b1 = pfma(tc, b2, padd(c0, pneg(b1)));
+        }
+#pragma unroll 1
+        for (; k > 0; --k, a -= 1024) {
+          const float2 nb2 = pfma(tc, b1, padd(lds2(a), pneg(b2)));
+          b2 = b1;
+          b1 = nb2;
+        }
+        // b1 = b_{k0}, b2 = b_{k0+1}
+        float res;
+        if (P.kbase == 1) {
+          res = fmaf(b1.x, c1, fmaf(b1.y, sn, -b2.x));
+        } else {
+          float sk, ck;
+          sincos_turns_n(g, P.invT, P.kbase, &sk, &ck);
+          const float cm = fmaf(ck, c1, sk * sn), sm = fmaf(sk, c1, -ck * sn);  // e^{i (k0-1) theta}
+          res = fmaf(b1.x, ck, fmaf(b1.y, sk, -fmaf(b2.x, cm, b2.y * sm)));
+        }
+        const int row = row0 + 2 * q + r;
+        const int col = 2 * (FUSE_COLS * cb_ - 2) + f;  // lanes 2..29 own f in [4, 60)
+        if (f >= 4 && f < 60 && col < P.Wf && row < Hf) {
+          float* sp = dbase + (long long)row * gpitch + col;
+          FLLF_DBG_STORE(P, sp, 4);
+          *sp = res;
+        }
+      }
     }
+    bar_sync_id(FUSE_BAR, nw * 32);
   }
 
   // One step t (pair P_{o0-2+t}): Wm, W0 = coarse rows j-3, j-2; Wn <- row
@@ -404,7 +404,7 @@ struct FuseWarp {
     if (VSTEP) vstep(d);
     if (VC) {
       if (P.exp & 2) {
-        if (++q == nb || t - 4 == R - 1) q = 0;
+        ++q;
       } else {
         coef(Wm, W0, Wn, Dm2e, Dm2o, Dm2g, t - 4, q);
       }
@@ -451,13 +451,17 @@ struct FuseWarp {
     step<true, true, true, false>(3, np, FUSE_PH0);
     int t = 4;
 #pragma unroll 1
-    for (; t + 2 <= R + 2; t += 3) {
+    for (; t + 2 <= R + 2; t += 3) {  // one batch (own pairs t-4 .. t-2) per iteration
+      q = 0;
       step<true, true, true, true>(t, np, FUSE_PH1);
       step<true, true, true, true>(t + 1, np, FUSE_PH2);
       step<true, true, true, true>(t + 2, np, FUSE_PH0);
+      order_sum(t - 4, FUSE_NB);
     }
-    // 0..2 steady steps remain (phase 1 first), then the last step t = R+3
+    // 0..2 steady steps remain (phase 1 first), then the last step t = R+3:
+    // the last (partial) batch
     const int rem = R + 3 - t;
+    q = 0;
     if (rem == 0) {
       step<true, false, false, true>(t, np, FUSE_PH1);
     } else if (rem == 1) {
@@ -468,6 +472,7 @@ struct FuseWarp {
       step<true, true, true, true>(t + 1, np, FUSE_PH2);
       step<true, false, false, true>(t + 2, np, FUSE_PH0);
     }
+    order_sum(t - 4, rem + 1);
 #undef FUSE_PH0
 #undef FUSE_PH1
 #undef FUSE_PH2
