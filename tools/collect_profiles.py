@@ -27,19 +27,19 @@ def kernels(src, dst):
     open(dst, "w").writelines(ln for ln in open(src) if ln.startswith("[bench]"))
 
 
-def launch_summary(tag, step_us):
+def launch_summary(tag, step_us, seqlen, workload):
     rows = [r for r in csv.reader(open(os.path.join(PROF, f"{tag}_launches.csv"))) if len(r) > 10]
     hdr = rows[0]
     ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
     ks = [(r[ki], float(r[vi].replace(",", ""))) for r in rows[1:] if "k_" in r[ki]]
-    seq = ks[-10:]
+    seq = ks[-seqlen:]
 
     def short(n):
         m = re.search(r"(k_\w+)(<[^>]*>)?", n)
         return (m.group(1) + (m.group(2) or "")) if m else n
 
     tot = sum(v for _, v in seq) / 1e3
-    md = ["# ncu launch list (bench.py --steps 2 --warmup 1, config2), last filter sequence", "",
+    md = [f"# ncu launch list (bench.py --steps 2 --warmup 1, {workload}), last filter sequence", "",
           "Cold-cache, serialised per-launch times (`--metrics gpu__time_duration.sum --clock-control none`). "
           "Compare shares, not absolutes.", "", "| # | kernel | us | share |", "|---|---|---|---|"]
     md += [f"| {i} | `{short(n)}` | {v / 1e3:.2f} | {v / 1e3 / tot:.1%} |" for i, (n, v) in enumerate(seq)]
@@ -47,29 +47,36 @@ def launch_summary(tag, step_us):
     open(os.path.join(PROF, f"{tag}_launches_summary.md"), "w").write("\n".join(md) + "\n")
 
 
+# one filter sequence of the default bench (config 5, 64 frames: design F on
+# levels 1-2, AB on 3-4) and of config 2 (design AB)
+SEQ_C5 = "build0,fuse1,fuse2,build3,build4,apply4,apply3,collapse2,collapse1,apply0"
+SEQ_C2 = "6"
+
+
 def main():
     tag = sys.argv[1]
     src = lambda n: os.path.join(OUT, f"{tag}_{n}")  # noqa: E731
     dst = lambda n: os.path.join(PROF, f"{tag}_{n}")  # noqa: E731
-    json_line(src("bench.json"), dst("bench_config2.json"))
-    kernels(src("bench.err"), dst("bench_config2_kernels.txt"))
-    for w in ("config5", "config4", "config3", "bands", "color"):
+    json_line(src("bench.json"), dst("bench_config5.json"))
+    kernels(src("bench.err"), dst("bench_config5_kernels.txt"))
+    for w in ("config2", "config4", "config3", "bands", "color"):
         if os.path.exists(src(f"bench_{w}.json")):
             json_line(src(f"bench_{w}.json"), dst(f"bench_{w}.json"))
-    if os.path.exists(src("bench_config5.err")):
-        kernels(src("bench_config5.err"), dst("bench_config5_kernels.txt"))
-    for n in ("reference.json", "launches.csv", "clocks.csv"):
+    if os.path.exists(src("bench_config2.err")):
+        kernels(src("bench_config2.err"), dst("bench_config2_kernels.txt"))
+    for n in ("reference.json", "launches.csv", "clocks.csv", "gpu_tests.log"):
         if os.path.exists(src(n)):
             shutil.copy(src(n), dst(n))
     import json
-    step_us = json.load(open(dst("bench_config2.json")))["ms_per_step"] * 1e3
-    launch_summary(tag, step_us)
+    step_us = json.load(open(dst("bench_config5.json")))["ms_per_step"] * 1e3
+    if os.path.exists(dst("launches.csv")):
+        launch_summary(tag, step_us, len(SEQ_C5.split(",")), "config5")
     summ = os.path.join(ROOT, "tools", "ncu_summary.py")
-    if os.path.exists(src("full.ncu-rep")):
-        subprocess.run([sys.executable, summ, src("full.ncu-rep"), dst("ncu_full_config2.md"), "config2", "6", "1"],
+    if os.path.exists(src("c5_full.ncu-rep")):  # 8 frames, the 64-frame bench's design
+        subprocess.run([sys.executable, summ, src("c5_full.ncu-rep"), dst("ncu_full_config5.md"), "config5", SEQ_C5, "8"],
                        check=True, stdout=subprocess.DEVNULL)
-    if os.path.exists(src("c5_full.ncu-rep")):  # tools/round_extra.sh captures 4 frames
-        subprocess.run([sys.executable, summ, src("c5_full.ncu-rep"), dst("ncu_full_config5.md"), "config5", "6", "4"],
+    if os.path.exists(src("c2_full.ncu-rep")):
+        subprocess.run([sys.executable, summ, src("c2_full.ncu-rep"), dst("ncu_full_config2.md"), "config2", SEQ_C2, "1"],
                        check=True, stdout=subprocess.DEVNULL)
     print("profiles written for", tag)
 

@@ -9,6 +9,7 @@ merged into profiles/roofline_traffic.json under "<workload>:<kind>:<level>";
 bench.py multiplies by its own batch for the roofline `traffic` field.
 """
 import csv
+import re
 import io
 import json
 import os
@@ -64,11 +65,20 @@ md = [f"# ncu --set full summary: `{os.path.basename(rep)}` ({workload})", "",
 open(out_md, "w").write("\n".join(md) + "\n")
 print("\n".join(md))
 if len(sys.argv) > 4:
-    levels = int(sys.argv[4])
-    order = [("build0", 0)] + [("build", l) for l in range(1, levels - 1)] + \
-            [("apply", l) for l in range(levels - 2, 0, -1)] + [("apply0", 0)]
-    vals = [v for k in seen for v in seen[k]]
-    # launches in report order
+    # argv[4]: the launch sequence of one filter, comma-separated kind+level
+    # (e.g. build0,fuse1,fuse2,build3,build4,apply4,apply3,collapse2,collapse1,apply0)
+    # or a level count for the design-AB order
+    spec = sys.argv[4]
+    if spec.isdigit():
+        levels = int(spec)
+        order = [("build0", 0)] + [("build", l) for l in range(1, levels - 1)] + \
+                [("apply", l) for l in range(levels - 2, 0, -1)] + [("apply0", 0)]
+    else:
+        order = []
+        for item in spec.split(","):
+            m = re.match(r"([a-z]+?)(\d+)$", item)
+            kind, lev = m.group(1), int(m.group(2))
+            order.append((kind if not (kind == "build" and lev == 0) else "build0", lev))
     rows_bytes = []
     for r in data:
         def mbv(k):
@@ -85,4 +95,3 @@ if len(sys.argv) > 4:
             tj[f"{workload}:{kind}:{lev}"] = round(b / frames)
         json.dump(tj, open(tp, "w"), indent=1, sort_keys=True)
         print("traffic ->", tp)
-

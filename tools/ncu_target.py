@@ -21,6 +21,8 @@ def main():
     ap.add_argument("--workload", default="config2")
     ap.add_argument("--iters", type=int, default=2)
     ap.add_argument("--frames", type=int, default=16)
+    ap.add_argument("--fused-levels", type=int, default=-1,
+                    help="design F on levels 1..N (0: AUTO for this batch; -1: as the 64-frame bench picks)")
     a = ap.parse_args()
     cfg = int(a.workload[-1])
     c = synth.CONFIGS[cfg]
@@ -35,6 +37,19 @@ def main():
     sig = c.get("sigma_r", 30.0)
     m = c.get("m", 2.0)
     with F.Plan(c["H"], c["W"], c["levels"], c["K"], c["T"], sig, m, batch=d_in.shape[0]) as p:
+        fl = a.fused_levels
+        if fl < 0:  # the bench's choice at its own batch: F on the levels with >= 4 MP over 64 frames
+            bench_batch = 64 if cfg == 5 else 1
+            fl, h, w = 0, c["H"], c["W"]
+            while fl < c["levels"] - 2:
+                h, w = (h + 1) // 2, (w + 1) // 2
+                if bench_batch * h * w < 4e6:
+                    break
+                fl += 1
+            if fl == 0:
+                F.fllf_plan_set_design(p.handle, F.FLLF_DESIGN_AB)
+        if fl > 0:
+            F.fllf_plan_set_fused_levels(p.handle, fl)
         for _ in range(a.iters):
             p.filter(d_in, d_out)
         torch.cuda.synchronize()
