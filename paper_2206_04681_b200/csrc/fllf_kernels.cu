@@ -1115,7 +1115,12 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
-template <bool LEVEL0, bool HAS_D, bool MAPS>
+// KT > 0: the plan's order count as a compile-time constant (level 0, SCALAR /
+// COEFFS, K = 8 or 16): the order loop unrolls completely, every coefficient
+// pair is an immediate constant-bank operand and the ring stages of a tile
+// are compile-time offsets from the tile's first stage (a tile uses K/2 of the
+// 8 stages, so it never wraps inside a tile).
+template <bool LEVEL0, bool HAS_D, bool MAPS, int KT = 0>
 __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0, MAPS>()) k_apply_cl(const __grid_constant__ ApplyParams P, const int ntiles) {
   constexpr int S = apply_cl_stages<LEVEL0, MAPS>();
   constexpr int HB = hdr_bytes<MAPS>();
@@ -1134,7 +1139,7 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0, MAPS>()) k_apply_cl
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
-  const int KL = P.KL;
+  const int KL = KT > 0 ? KT : P.KL;
   // g rows by TMA: internal planes always; the caller's image when its rows
   // are 16-byte aligned and W is a multiple of 4 (copies never leave a row)
   const bool tma_g = !LEVEL0 || (((reinterpret_cast<uintptr_t>(P.img.p) & 15) == 0) &&
@@ -1441,7 +1446,26 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0, MAPS>()) k_apply_cl
     };
 
     int i = KL - 1;
-    if (OPS == 2) {
+    constexpr bool kFull = KT > 0 && OPS == 2 && (KT % 2) == 0 && (S % (KT / 2)) == 0;
+    if constexpr (kFull) {
+      const unsigned char* rs = rowc + s * STAGE;
+      const uint32_t fb = smem_u32(&full[s]), eb = smem_u32(&empty[s]);
+#pragma unroll
+      for (int jst = 0; jst < KT / 2; ++jst) {
+        mbar_wait_u32(fb + jst * 8, ph);
+        const unsigned char* so = rs + jst * STAGE;
+        order(KT - 1 - 2 * jst, so, b2, b1);
+        order(KT - 2 - 2 * jst, so + OBYTES, b1, b2);
+        __syncwarp();
+        if (lane == 0) mbar_arrive_u32(eb + jst * 8);
+      }
+      s += KT / 2;
+      if (s == S) {
+        s = 0;
+        ph ^= 1u;
+      }
+      i = -1;
+    } else if (OPS == 2) {
       constexpr int UNR = MAPS ? 1 : kApply0Unroll;  // MAPS: unrolling measured slower
 #pragma unroll UNR
       for (; i >= 1; i -= 2) {
@@ -1686,15 +1710,28 @@ static cudaError_t launch_apply_t(const ApplyParams& p, int batch, cudaStream_t 
   return launch_ex(k_apply<L0, HD, MP>, grid, dim3(160), smem, s, pdl, p, ntiles);
 }
 
-template <bool L0, bool HD, bool MP>
-static cudaError_t launch_apply_cl_t(const ApplyParams& p, int batch, cudaStream_t s, bool pdl) {
+template <bool L0, bool HD, bool MP, int KT = 0>
+static cudaError_t launch_apply_cl_k(const ApplyParams& p, int batch, cudaStream_t s, bool pdl) {
   const int ntiles = ((p.Wf + 119) / 120) * ((p.r_end - p.r_begin + 3) / 4) * batch;
   dim3 grid(std::min(ntiles, sm_count() * apply_cl_ctas<L0, MP>()));
   const int smem = apply_cl_smem<L0, MP>();
   static DeviceFlags attr_set;
-  cudaError_t e = smem_opt_in(k_apply_cl<L0, HD, MP>, smem, attr_set);
+  cudaError_t e = smem_opt_in(k_apply_cl<L0, HD, MP, KT>, smem, attr_set);
   if (e != cudaSuccess) return e;
-  return launch_ex(k_apply_cl<L0, HD, MP>, grid, dim3(160), smem, s, pdl, p, ntiles);
+  return launch_ex(k_apply_cl<L0, HD, MP, KT>, grid, dim3(160), smem, s, pdl, p, ntiles);
+}
+
+template <bool L0, bool HD, bool MP>
+static cudaError_t launch_apply_cl_t(const ApplyParams& p, int batch, cudaStream_t s, bool pdl) {
+  static const bool generic = [] {  // FLLF_APPLY0_GENERIC=1: no order-count specialisation (A/B)
+    const char* e = std::getenv("FLLF_APPLY0_GENERIC");
+    return e && e[0] == '1';
+  }();
+  if constexpr (L0 && !MP) {
+    if (!generic && p.KL == 16) return launch_apply_cl_k<L0, HD, MP, 16>(p, batch, s, pdl);
+    if (!generic && p.KL == 8) return launch_apply_cl_k<L0, HD, MP, 8>(p, batch, s, pdl);
+  }
+  return launch_apply_cl_k<L0, HD, MP>(p, batch, s, pdl);
 }
 
 cudaError_t launch_apply(const ApplyParams& p, int level_fine, bool has_d, bool maps, int batch,
