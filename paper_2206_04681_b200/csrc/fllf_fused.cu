@@ -124,12 +124,14 @@ struct FuseLayout {
 
 // ---- one warp: NC orders of the strip (DO_G: warp 0 also builds G;
 // ROWS_IN: no fine row of the strip needs reflection)
-template <int NC, int PD, bool EDGE, bool DO_G, bool ROWS_IN>
+template <int NC, int PD, bool EDGE, bool DO_G, bool ROWS_IN, int KT>
 struct FuseWarp {
   using L = FuseLayout<NC, PD>;
   static constexpr int DEPTH = L::DEPTH;
   static constexpr int SLOT = DO_G ? L::G0SLOT : L::ZSLOT;
   static constexpr int ZOFF = DO_G ? 512 : 0;
+  // the plan's order count (compile time for KT > 0)
+  __device__ __forceinline__ int kl() const { return KT > 0 ? KT : P.KL; }
 
   const FuseParams& P;
   int o0, R, lane, warp, nw, nb;
@@ -174,10 +176,10 @@ struct FuseWarp {
     zsrc = P.src.Z + frame * P.src.fstride_z + (long long)il0 * zks + r0 * zpitch + (EDGE ? 0 : c0);
     gout = P.dst.G + frame * P.dst.fstride_r + (long long)(o0 - 1) * P.dst.pitch + x;
     zout = P.dst.Z + frame * P.dst.fstride_z + (long long)il0 * P.dst.kstride_z + (long long)(o0 - 1) * P.dst.zpitch + x;
-    ring = smem + L::ring_off(P.KL, warp);
+    ring = smem + L::ring_off(kl(), warp);
     si = sr = 0;
     crow = smem + il0 * 1024 + lane * 16;
-    gbrow = smem + L::g_off(P.KL) + lane * 8;
+    gbrow = smem + L::g_off(kl()) + lane * 8;
     jn = o0 - 2;
 #pragma unroll
     for (int i = 0; i < NC; ++i) {
@@ -306,7 +308,7 @@ struct FuseWarp {
   __device__ __forceinline__ void coef(const float2 (&Cm)[NC], const float2 (&C0)[NC], const float2 (&Cp)[NC],
                                        const float4 (&ze)[NC], const float4 (&zo)[NC], const float4& gg, int n,
                                        int& q) {
-    const uint32_t cb = crow + q * (P.KL * 1024);
+    const uint32_t cb = crow + q * (kl() * 1024);
 #pragma unroll
     for (int i = 0; i < NC; ++i) {
       // vertical up-sampling (unscaled): even fine row x_{i-1} + 6 x_i + x_{i+1}, odd x_i + x_{i+1}
@@ -340,7 +342,7 @@ struct FuseWarp {
   __device__ __forceinline__ void order_sum(int n0, int cnt) {
     bar_sync_id(FUSE_BAR, nw * 32);
     if (!(P.exp & 1)) {
-      const int KL = P.KL;
+      const int KL = kl();
       const int goff = L::g_off(KL);
       const int row0 = 2 * (o0 + n0);
 #pragma unroll 1
@@ -353,7 +355,7 @@ struct FuseWarp {
         float2 b1 = make_float2(0.f, 0.f), b2 = b1;
         uint32_t a = sbase_ + ((q * KL + KL - 1) * 2 + r) * 512 + f * 8;
         int k = KL;
-#pragma unroll 1
+#pragma unroll(KT > 0 ? 8 : 1)
         for (; k >= 4; k -= 4, a -= 4096) {
           const float2 c3 = lds2(a), c2 = lds2(a - 1024), c1v = lds2(a - 2048), c0 = lds2(a - 3072);
           b2 = pfma(tc, b1, padd(c3, pneg(b2)));
@@ -480,19 +482,21 @@ struct FuseWarp {
   }
 };
 
-template <int NC, int PD, bool EDGE, bool ROWS_IN>
+template <int NC, int PD, bool EDGE, bool ROWS_IN, int KT>
 __device__ __forceinline__ void fuse_run(const FuseParams& P, int cb, int o0, int R, int frame, int nw, int warp,
                                          uint32_t sbase) {
   if (warp == 0) {
-    FuseWarp<NC, PD, EDGE, true, ROWS_IN> w(P, cb, o0, R, frame, nw, warp, sbase);
+    FuseWarp<NC, PD, EDGE, true, ROWS_IN, KT> w(P, cb, o0, R, frame, nw, warp, sbase);
     w.run();
   } else {
-    FuseWarp<NC, PD, EDGE, false, ROWS_IN> w(P, cb, o0, R, frame, nw, warp, sbase);
+    FuseWarp<NC, PD, EDGE, false, ROWS_IN, KT> w(P, cb, o0, R, frame, nw, warp, sbase);
     w.run();
   }
 }
 
-template <int NC, int PD>
+// KT > 0: the plan's order count at compile time (16 or 8; the order sums'
+// Clenshaw loop unrolls completely, the layout offsets fold)
+template <int NC, int PD, int KT = 0>
 __global__ void __launch_bounds__(FUSE_MAX_WARPS * 32, 1) k_fuse(const __grid_constant__ FuseParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   pdl_wait();     // level l (G_l, Z_l) is complete
@@ -502,18 +506,18 @@ __global__ void __launch_bounds__(FUSE_MAX_WARPS * 32, 1) k_fuse(const __grid_co
   const int o0 = blockIdx.y * P.rows_per_strip;
   const int R = min(P.rows_per_strip, P.Hc - o0);
   const int frame = blockIdx.z;
-  const int nw = P.KL / NC;
+  const int nw = (KT > 0 ? KT : P.KL) / NC;
   const int warp = threadIdx.x >> 5;
   // all 64 fine columns of the warp inside the row: no per-lane reflection
   const bool interior = cb >= 1 && 2 * FUSE_COLS * cb + 60 <= P.Wf;
   // pairs o0-2 .. o0+R+1 inside the frame: no row reflection
   const bool rows_in = o0 >= 2 && 2 * (o0 + R + 1) + 1 < P.Hf;
   if (interior) {
-    if (rows_in) fuse_run<NC, PD, false, true>(P, cb, o0, R, frame, nw, warp, sbase);
-    else fuse_run<NC, PD, false, false>(P, cb, o0, R, frame, nw, warp, sbase);
+    if (rows_in) fuse_run<NC, PD, false, true, KT>(P, cb, o0, R, frame, nw, warp, sbase);
+    else fuse_run<NC, PD, false, false, KT>(P, cb, o0, R, frame, nw, warp, sbase);
   } else {
-    if (rows_in) fuse_run<NC, PD, true, true>(P, cb, o0, R, frame, nw, warp, sbase);
-    else fuse_run<NC, PD, true, false>(P, cb, o0, R, frame, nw, warp, sbase);
+    if (rows_in) fuse_run<NC, PD, true, true, KT>(P, cb, o0, R, frame, nw, warp, sbase);
+    else fuse_run<NC, PD, true, false, KT>(P, cb, o0, R, frame, nw, warp, sbase);
   }
 }
 
@@ -594,11 +598,20 @@ cudaError_t launch_fuse_nc(const FuseParams& p0, int batch, cudaStream_t s, bool
   }();
   p.exp = exp;
   const int smem = FuseLayout<NC, PD>::smem(p.KL);
-  static DeviceFlags attr_set;
-  cudaError_t e = smem_opt_in(k_fuse<NC, PD>, kFuseSmemMax, attr_set);
-  if (e != cudaSuccess) return e;
   dim3 grid(bx, (p.Hc + R - 1) / R, batch);
-  return launch_ex(k_fuse<NC, PD>, grid, dim3(32 * (p.KL / NC)), smem, s, pdl, p);
+  const dim3 block(32 * (p.KL / NC));
+  static DeviceFlags attr0, attr8, attr16;
+  cudaError_t e;
+  if (NC == 1 && p.KL == 16) {
+    if ((e = smem_opt_in(k_fuse<NC, PD, 16>, kFuseSmemMax, attr16)) != cudaSuccess) return e;
+    return launch_ex(k_fuse<NC, PD, 16>, grid, block, smem, s, pdl, p);
+  }
+  if (NC == 1 && p.KL == 8) {
+    if ((e = smem_opt_in(k_fuse<NC, PD, 8>, kFuseSmemMax, attr8)) != cudaSuccess) return e;
+    return launch_ex(k_fuse<NC, PD, 8>, grid, block, smem, s, pdl, p);
+  }
+  if ((e = smem_opt_in(k_fuse<NC, PD>, kFuseSmemMax, attr0)) != cudaSuccess) return e;
+  return launch_ex(k_fuse<NC, PD>, grid, block, smem, s, pdl, p);
 }
 
 }  // namespace
