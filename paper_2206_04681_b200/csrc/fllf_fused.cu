@@ -565,7 +565,7 @@ __global__ void __launch_bounds__(128) k_collapse(const CollapseParams P) {
 constexpr int kFuseSmemMax = 227 * 1024;
 // ring depth (pairs ahead): 4 with one order per warp, 2 with two (shared memory)
 #ifndef FLLF_FUSE_PD1
-#define FLLF_FUSE_PD1 4
+#define FLLF_FUSE_PD1 6
 #endif
 template <int NC>
 constexpr int fuse_pd() {
