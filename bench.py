@@ -285,6 +285,17 @@ def run_adaptive(args, c, wl, world, rank, local):
     clk.stop()
     b_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
     a_ms = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps / len(maps)
+    # per-kernel durations of one reapply per map (events around every launch;
+    # outside the timed region, stderr only)
+    F.fllf_plan_set_profiling(plan.handle, True)
+    per_kernel = {}
+    for s_map, m_map in maps:
+        plan.apply(out, mode=F.FLLF_MAPS, sigma_map=s_map, m_map=m_map, stream=stream)
+        for kind, lev, ms in F.fllf_plan_kernel_times(plan.handle):
+            per_kernel.setdefault((kind, lev), []).append(ms)
+    F.fllf_plan_set_profiling(plan.handle, False)
+    for (kind, lev), v in sorted(per_kernel.items(), key=lambda kv: -sum(kv[1])):
+        log(f"[bench] {kind:7s} l={lev}  avg {sum(v) / len(v) * 1e3:8.2f} us per reapply")
     tot = torch.tensor([sum(e[0].elapsed_time(e[2]) for e in evs)], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)

@@ -733,6 +733,8 @@ static fllf_status apply_impl(fllf_plan p, const fllf_apply_args* a, float* d_ou
     ap.wk[i][2] = make_float2(-ap.a[i] / 16.f, -ap.a[i] / 16.f);
     ap.wk[i][3] = make_float2(-ap.a[i] / 4.f, -ap.a[i] / 4.f);
     clenshaw_pairs(a, ap.cw[i]);
+    // MAPS (k_apply_cl): (k^2, log2 k) of the global order k
+    if (mode == FLLF_MAPS) ap.cw[i][0] = make_float2(a * a, (float)std::log2((double)(p->kb + i)));
   }
   int launches = 0;
   if (p->last_was_apply) p->nrec = 0;

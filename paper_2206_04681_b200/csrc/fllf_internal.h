@@ -103,6 +103,7 @@ struct ApplyParams {
   // sum_k (c_cos cos k theta + c_sin sin k theta):
   // [0] = (-a/64, a/64) even row, even col; [1] = (-a/16, a/16) mixed;
   // [2] = (-a/4, a/4) odd row, odd col; [3] = (a, -a) same-level Z (l >= 1).
+  // MAPS: [0] = (k^2, log2 k) of the global order k (a_k is per pixel).
   float2 cw[FLLF_MAX_K][4];
   // Row bands (see BuildParams): tiles cover the coarse rows [r_begin, r_end);
   // coarse-plane (Z_{l+1}, D_{l+1}) reads are clamped to [cr_lo, cr_hi],

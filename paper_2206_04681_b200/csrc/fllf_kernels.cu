@@ -1353,22 +1353,33 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0, MAPS>()) k_apply_cl
       sincos_turns(g[p], P.invT, &sn[p], &c);
       tc[p] = 2.f * c;
     }
-    // MAPS (Sec. III-B): a_k(p) = m sigma^3 c0 k exp(-k^2 hq sigma^2) = Am[p] k 2^(k^2 Bm[p]);
-    // the factor k sits in P.cw (built with a_k := k), the rest per pixel and order
-    float Am[8], Bm[8];
+    // MAPS (Sec. III-B): a_k(p) = m sigma^3 c0 k exp(-k^2 hq sigma^2).  Per
+    // pixel and order ONE exp2 of  k^2 Bm[p] + Lm[p] + log2 k  with
+    // Bm = -hq log2(e) sigma^2 and Lm = log2(sigma^3 c0) (+ log2 of the
+    // polyphase up-sampling scale at level 0); the factor m multiplies the
+    // finished order sum (it is linear in the a_k).  Bm / Lm packed over the
+    // pixel pairs (2q, 2q+1); (k^2, log2 k) per order in P.cw[i][0].
+    float2 Bm[4], Lm[4];
     if (MAPS) {
       mbar_wait_parity(&mfull[hb], hph);
+      const float lc0 = __log2f(P.c0);
 #pragma unroll
       for (int tt = 0; tt < 2; ++tt) {
         const float4 sv = *reinterpret_cast<const float4*>(hdr + HDR_S_OFF + (2 * warp + tt) * HDR_G_ROW + lg * 16);
-        const float4 mv = *reinterpret_cast<const float4*>(hdr + HDR_M_OFF + (2 * warp + tt) * HDR_G_ROW + lg * 16);
-        const float sg[4] = {sv.x, sv.y, sv.z, sv.w}, mm[4] = {mv.x, mv.y, mv.z, mv.w};
+        const float sg[4] = {sv.x, sv.y, sv.z, sv.w};
+        float bq[4], lq[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const float s2 = sg[q] * sg[q];
-          Am[4 * tt + q] = mm[q] * s2 * sg[q] * P.c0;
-          Bm[4 * tt + q] = -P.hq * 1.4426950408889634f * s2;
+          bq[q] = -P.hq * 1.4426950408889634f * (sg[q] * sg[q]);
+          // level 0: the scale 1/64, 1/16 (even row) and 1/16, 1/4 (odd row) of
+          // pixel (even, odd) column, as P.cw[i][0..2] carries it for SCALAR
+          const float ls = LEVEL0 ? (tt == 0 ? ((q & 1) ? -4.f : -6.f) : ((q & 1) ? -2.f : -4.f)) : 0.f;
+          lq[q] = fmaf(3.f, __log2f(sg[q]), lc0 + ls);
         }
+        Bm[2 * tt] = make_float2(bq[0], bq[1]);
+        Bm[2 * tt + 1] = make_float2(bq[2], bq[3]);
+        Lm[2 * tt] = make_float2(lq[0], lq[1]);
+        Lm[2 * tt + 1] = make_float2(lq[2], lq[3]);
       }
     }
     float2 b1[8], b2[8];
@@ -1405,31 +1416,40 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0, MAPS>()) k_apply_cl
       raw[5] = padd(voa, vob);
       raw[6] = pfma(bc(6.f), vob, padd(voa, Ro));
       raw[7] = padd(vob, Ro);
-      const float2 w64 = P.cw[i][0], w16 = P.cw[i][1], w4 = P.cw[i][2];
-      float kk2 = 0.f;
-      if (MAPS) {
-        const float kk = (float)(P.kbase + i);
-        kk2 = kk * kk;
-      }
+      if constexpr (MAPS) {
+        // sign convention of the MAPS recurrence: the cosine component carries
+        // -b (c_cos = -a Im(.) becomes +a Im(.)), undone at the end; then
+        // c = a_k(p)/m * (s raw - fine Z) in both components
+        const float2 mk = P.cw[i][0];  // (k^2, log2 k)
+        float2 ea[4];
 #pragma unroll
-      for (int p = 0; p < 8; ++p) {
-        const float2 w = (p < 4) ? ((p & 1) ? w16 : w64) : ((p & 1) ? w4 : w16);
-        float2 c;
-        if (MAPS) {
-          c = pmul(raw[p], w);
-          if (!LEVEL0) {
-            const float4 fv = fz[(p >> 2) * 2 + ((p & 3) >> 1)];
-            c = pfma((p & 1) ? hi2(fv) : lo2(fv), P.cw[i][3], c);
-          }
-          c = pfma(c, bc(Am[p] * ex2_approx(kk2 * Bm[p])), pneg(bn[p]));
-        } else {
-          c = pfma(raw[p], w, pneg(bn[p]));
-          if (!LEVEL0) {
-            const float4 fv = fz[(p >> 2) * 2 + ((p & 3) >> 1)];
-            c = pfma((p & 1) ? hi2(fv) : lo2(fv), P.cw[i][3], c);
-          }
+        for (int q = 0; q < 4; ++q) {
+          const float2 arg = pfma(bc(mk.x), Bm[q], padd(Lm[q], bc(mk.y)));
+          ea[q] = make_float2(ex2_approx(arg.x), ex2_approx(arg.y));
         }
-        bn[p] = pfma(bc(tc[p]), bp[p], c);
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+          const float e = (p & 1) ? ea[p >> 1].y : ea[p >> 1].x;
+          float2 d = raw[p];
+          if (!LEVEL0) {
+            const float sc = (p < 4) ? ((p & 1) ? 1.f / 16.f : 1.f / 64.f) : ((p & 1) ? 0.25f : 1.f / 16.f);
+            const float4 fv = fz[(p >> 2) * 2 + ((p & 3) >> 1)];
+            d = pfma(bc(sc), raw[p], pneg((p & 1) ? hi2(fv) : lo2(fv)));
+          }
+          bn[p] = pfma(bc(tc[p]), bp[p], pfma(d, bc(e), pneg(bn[p])));
+        }
+      } else {
+        const float2 w64 = P.cw[i][0], w16 = P.cw[i][1], w4 = P.cw[i][2];
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+          const float2 w = (p < 4) ? ((p & 1) ? w16 : w64) : ((p & 1) ? w4 : w16);
+          float2 c = pfma(raw[p], w, pneg(bn[p]));
+          if (!LEVEL0) {
+            const float4 fv = fz[(p >> 2) * 2 + ((p & 3) >> 1)];
+            c = pfma((p & 1) ? hi2(fv) : lo2(fv), P.cw[i][3], c);
+          }
+          bn[p] = pfma(bc(tc[p]), bp[p], c);
+        }
       }
     };
     auto stage_wait = [&]() -> const unsigned char* {
@@ -1494,6 +1514,13 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0, MAPS>()) k_apply_cl
       }
     }
     // b1 = b_{k0}, b2 = b_{k0+1}
+    if constexpr (MAPS) {  // back to the common sign convention
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        b1[p].x = -b1[p].x;
+        b2[p].x = -b2[p].x;
+      }
+    }
     float res[8];
     if (P.kbase == 1) {
 #pragma unroll
@@ -1506,6 +1533,16 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0, MAPS>()) k_apply_cl
         const float c1 = 0.5f * tc[p], s1 = sn[p];
         const float cm = fmaf(ck, c1, sk * s1), sm = fmaf(sk, c1, -ck * s1);  // e^{i (k0-1) theta}
         res[p] = fmaf(b1[p].x, ck, fmaf(b1[p].y, sk, -fmaf(b2[p].x, cm, b2[p].y * sm)));
+      }
+    }
+    if constexpr (MAPS) {  // the factor m of a_k (header rows, still held)
+#pragma unroll
+      for (int tt = 0; tt < 2; ++tt) {
+        const float4 mv = *reinterpret_cast<const float4*>(hdr + HDR_M_OFF + (2 * warp + tt) * HDR_G_ROW + lg * 16);
+        res[4 * tt + 0] *= mv.x;
+        res[4 * tt + 1] *= mv.y;
+        res[4 * tt + 2] *= mv.z;
+        res[4 * tt + 3] *= mv.w;
       }
     }
 

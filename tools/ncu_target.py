@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--workload", default="config2")
     ap.add_argument("--iters", type=int, default=2)
     ap.add_argument("--frames", type=int, default=16)
+    ap.add_argument("--maps", action="store_true", help="config 4: build once, then one MAPS apply")
     ap.add_argument("--fused-levels", type=int, default=-1,
                     help="design F on levels 1..N (0: AUTO for this batch; -1: as the 64-frame bench picks)")
     a = ap.parse_args()
@@ -37,6 +38,14 @@ def main():
     sig = c.get("sigma_r", 30.0)
     m = c.get("m", 2.0)
     with F.Plan(c["H"], c["W"], c["levels"], c["K"], c["T"], sig, m, batch=d_in.shape[0]) as p:
+        if a.maps:
+            s_map, m_map = (torch.from_numpy(v).cuda() for v in synth.config4_maps(0, H=c["H"], W=c["W"]))
+            p.build(d_in)
+            for _ in range(a.iters):
+                p.apply(d_out, mode=F.FLLF_MAPS, sigma_map=s_map, m_map=m_map)
+            torch.cuda.synchronize()
+            print("MAPS apply ok, out mean", float(d_out.mean()))
+            return
         fl = a.fused_levels
         if fl < 0:  # the bench's choice at its own batch: F on the levels with >= 4 MP over 64 frames
             bench_batch = 64 if cfg == 5 else 1
