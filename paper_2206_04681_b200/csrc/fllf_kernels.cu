@@ -1100,13 +1100,16 @@ constexpr int kApply0Unroll = FLLF_A0_UNROLL;
 #define FLLF_A1_UNROLL 1
 #endif
 constexpr int kApply1Unroll = FLLF_A1_UNROLL;  // levels >= 1 (A/B knob)
-template <bool LEVEL0, bool MAPS = false>
+// KT > 0 (level 0): a whole tile's orders in a ring of K/2 stages when that
+// is 6..8 (the ring then restarts at the same stage every tile)
+template <bool LEVEL0, bool MAPS = false, int KT = 0>
 __host__ __device__ constexpr int apply_cl_stages() {
-  return LEVEL0 ? (FLLF_APPLY0_CTAS >= 4 ? 6 : 8) : (MAPS ? (FLLF_MAPS1_CTAS <= 2 ? 6 : 4) : 5);
+  return (LEVEL0 && KT == 12) ? 6
+                              : (LEVEL0 ? (FLLF_APPLY0_CTAS >= 4 ? 6 : 8) : (MAPS ? (FLLF_MAPS1_CTAS <= 2 ? 6 : 4) : 5));
 }
-template <bool LEVEL0, bool MAPS = false>
+template <bool LEVEL0, bool MAPS = false, int KT = 0>
 __host__ __device__ constexpr int apply_cl_smem() {
-  return apply_cl_stages<LEVEL0, MAPS>() * apply_cl_ops<LEVEL0>() * apply_stage_bytes<LEVEL0>() + 2 * hdr_bytes<MAPS>();
+  return apply_cl_stages<LEVEL0, MAPS, KT>() * apply_cl_ops<LEVEL0>() * apply_stage_bytes<LEVEL0>() + 2 * hdr_bytes<MAPS>();
 }
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -1122,7 +1125,7 @@ __device__ __forceinline__ float ex2_approx(float x) {
 // 8 stages, so it never wraps inside a tile).
 template <bool LEVEL0, bool HAS_D, bool MAPS, int KT = 0>
 __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0, MAPS>()) k_apply_cl(const __grid_constant__ ApplyParams P, const int ntiles) {
-  constexpr int S = apply_cl_stages<LEVEL0, MAPS>();
+  constexpr int S = apply_cl_stages<LEVEL0, MAPS, KT>();
   constexpr int HB = hdr_bytes<MAPS>();
   constexpr int OPS = apply_cl_ops<LEVEL0>();
   constexpr int OBYTES = apply_stage_bytes<LEVEL0>();  // one order
@@ -1751,7 +1754,7 @@ template <bool L0, bool HD, bool MP, int KT = 0>
 static cudaError_t launch_apply_cl_k(const ApplyParams& p, int batch, cudaStream_t s, bool pdl) {
   const int ntiles = ((p.Wf + 119) / 120) * ((p.r_end - p.r_begin + 3) / 4) * batch;
   dim3 grid(std::min(ntiles, sm_count() * apply_cl_ctas<L0, MP>()));
-  const int smem = apply_cl_smem<L0, MP>();
+  const int smem = apply_cl_smem<L0, MP, KT>();
   static DeviceFlags attr_set;
   cudaError_t e = smem_opt_in(k_apply_cl<L0, HD, MP, KT>, smem, attr_set);
   if (e != cudaSuccess) return e;
@@ -1767,6 +1770,9 @@ static cudaError_t launch_apply_cl_t(const ApplyParams& p, int batch, cudaStream
   if constexpr (L0 && !MP) {
     if (!generic && p.KL == 16) return launch_apply_cl_k<L0, HD, MP, 16>(p, batch, s, pdl);
     if (!generic && p.KL == 8) return launch_apply_cl_k<L0, HD, MP, 8>(p, batch, s, pdl);
+  }
+  if constexpr (L0 && MP) {  // BASELINE configs[3]: K = 12
+    if (!generic && p.KL == 12) return launch_apply_cl_k<L0, HD, MP, 12>(p, batch, s, pdl);
   }
   return launch_apply_cl_k<L0, HD, MP>(p, batch, s, pdl);
 }
