@@ -522,42 +522,65 @@ __global__ void __launch_bounds__(FUSE_MAX_WARPS * 32, 1) k_fuse(const __grid_co
 }
 
 // D_l += up(D_{l+1}) (polyphase up-sampling with the border rule of upmap):
-// one thread per coarse pixel = a 2x2 block of fine pixels.
+// one thread per 2 x 2 coarse pixels = a 4 x 4 block of fine pixels (16
+// coarse loads for 4 coarse pixels, four independent 16-byte read-modify-
+// writes of the fine rows).  Same arithmetic per fine pixel as one thread
+// per coarse pixel: vertical (x_{r-1} + 6 x_r + x_{r+1}) / 8 | (x_r + x_{r+1}) / 2,
+// then the same horizontally.
 __global__ void __launch_bounds__(128) k_collapse(const CollapseParams P) {
   pdl_wait();  // D_{l+1} is complete
   pdl_trigger();
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int r = blockIdx.y;
-  if (x >= P.Wc) return;
+  const int x0 = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+  const int r0 = 2 * blockIdx.y;
+  if (x0 >= P.Wc) return;
   const float* dc = P.coarse + blockIdx.z * P.cfstride;
   float* df = P.fine + blockIdx.z * P.ffstride;
-  const int xs[3] = {upmap(x - 1, P.Wc, P.Wf), x, upmap(x + 1, P.Wc, P.Wf)};
-  const int rs[3] = {upmap(r - 1, P.Hc, P.Hf), r, upmap(r + 1, P.Hc, P.Hf)};
-  float ve[3], vo[3];
+  int xs[4], rs[4];
 #pragma unroll
-  for (int b = 0; b < 3; ++b) {
-    const float d0 = __ldg(dc + (long long)rs[0] * P.cpitch + xs[b]);
-    const float d1 = __ldg(dc + (long long)rs[1] * P.cpitch + xs[b]);
-    const float d2 = __ldg(dc + (long long)rs[2] * P.cpitch + xs[b]);
-    ve[b] = fmaf(6.f, d1, d0 + d2) * 0.125f;
-    vo[b] = (d1 + d2) * 0.5f;
+  for (int j = 0; j < 4; ++j) {
+    xs[j] = upmap(x0 - 1 + j, P.Wc, P.Wf);
+    rs[j] = upmap(r0 - 1 + j, P.Hc, P.Hf);
   }
-  const float o[2][2] = {{fmaf(6.f, ve[1], ve[0] + ve[2]) * 0.125f, (ve[1] + ve[2]) * 0.5f},
-                         {fmaf(6.f, vo[1], vo[0] + vo[2]) * 0.125f, (vo[1] + vo[2]) * 0.5f}};
+  float d[4][4];  // [coarse row r0-1+i][coarse column x0-1+j]
 #pragma unroll
-  for (int t = 0; t < 2; ++t) {
-    const int row = 2 * r + t;
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) d[i][j] = __ldg(dc + (long long)rs[i] * P.cpitch + xs[j]);
+  // vertical: fine rows 2 r0 + t, t = 0..3 (coarse rows r0, r0 + 1; even / odd)
+  float v[4][4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    v[0][j] = fmaf(6.f, d[1][j], d[0][j] + d[2][j]) * 0.125f;
+    v[1][j] = (d[1][j] + d[2][j]) * 0.5f;
+    v[2][j] = fmaf(6.f, d[2][j], d[1][j] + d[3][j]) * 0.125f;
+    v[3][j] = (d[2][j] + d[3][j]) * 0.5f;
+  }
+  const bool vec = ((reinterpret_cast<uintptr_t>(df) & 15) == 0) && ((P.fpitch & 3) == 0) && 2 * x0 + 3 < P.Wf;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int row = 2 * r0 + t;
     if (row >= P.Hf) break;
-    float* fp = df + (long long)row * P.fpitch + 2 * x;
-    if (2 * x + 1 < P.Wf) {
-      FLLF_DBG_STORE(P, fp, 8);
-      float2 v = *reinterpret_cast<float2*>(fp);
-      v.x += o[t][0];
-      v.y += o[t][1];
-      *reinterpret_cast<float2*>(fp) = v;
+    const float o0 = fmaf(6.f, v[t][1], v[t][0] + v[t][2]) * 0.125f;
+    const float o1 = (v[t][1] + v[t][2]) * 0.5f;
+    const float o2 = fmaf(6.f, v[t][2], v[t][1] + v[t][3]) * 0.125f;
+    const float o3 = (v[t][2] + v[t][3]) * 0.5f;
+    float* fp = df + (long long)row * P.fpitch + 2 * x0;
+    if (vec) {
+      FLLF_DBG_STORE(P, fp, 16);
+      float4 q = *reinterpret_cast<float4*>(fp);
+      q.x += o0;
+      q.y += o1;
+      q.z += o2;
+      q.w += o3;
+      *reinterpret_cast<float4*>(fp) = q;
     } else {
-      FLLF_DBG_STORE(P, fp, 4);
-      fp[0] += o[t][0];
+      const float o[4] = {o0, o1, o2, o3};
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (2 * x0 + u < P.Wf) {
+          FLLF_DBG_STORE(P, fp + u, 4);
+          fp[u] += o[u];
+        }
     }
   }
 }
@@ -631,7 +654,7 @@ cudaError_t launch_fuse(const FuseParams& p, int batch, cudaStream_t s, bool pdl
 }
 
 cudaError_t launch_collapse(const CollapseParams& p, int batch, cudaStream_t s, bool pdl) {
-  dim3 grid((p.Wc + 127) / 128, p.Hc, batch);
+  dim3 grid(((p.Wc + 1) / 2 + 127) / 128, (p.Hc + 1) / 2, batch);
   return launch_ex(k_collapse, grid, dim3(128), 0, s, pdl, p);
 }
 
