@@ -62,8 +62,9 @@ def main():
     for w in ("config2", "config4", "config3", "bands", "color"):
         if os.path.exists(src(f"bench_{w}.json")):
             json_line(src(f"bench_{w}.json"), dst(f"bench_{w}.json"))
-    if os.path.exists(src("bench_config2.err")):
-        kernels(src("bench_config2.err"), dst("bench_config2_kernels.txt"))
+    for w in ("config2", "config4"):
+        if os.path.exists(src(f"bench_{w}.err")):
+            kernels(src(f"bench_{w}.err"), dst(f"bench_{w}_kernels.txt"))
     for n in ("reference.json", "launches.csv", "clocks.csv", "gpu_tests.log"):
         if os.path.exists(src(n)):
             shutil.copy(src(n), dst(n))
@@ -73,10 +74,12 @@ def main():
         launch_summary(tag, step_us, len(SEQ_C5.split(",")), "config5")
     summ = os.path.join(ROOT, "tools", "ncu_summary.py")
     if os.path.exists(src("c5_full.ncu-rep")):  # 8 frames, the 64-frame bench's design
-        subprocess.run([sys.executable, summ, src("c5_full.ncu-rep"), dst("ncu_full_config5.md"), "config5", SEQ_C5, "8"],
+        subprocess.run([sys.executable, summ, src("c5_full.ncu-rep"), dst("ncu_full_config5.md"), "config5", SEQ_C5, "8",
+                        str(1080 * 1920)],
                        check=True, stdout=subprocess.DEVNULL)
     if os.path.exists(src("c2_full.ncu-rep")):
-        subprocess.run([sys.executable, summ, src("c2_full.ncu-rep"), dst("ncu_full_config2.md"), "config2", SEQ_C2, "1"],
+        subprocess.run([sys.executable, summ, src("c2_full.ncu-rep"), dst("ncu_full_config2.md"), "config2", SEQ_C2, "1",
+                        str(1080 * 1920)],
                        check=True, stdout=subprocess.DEVNULL)
     print("profiles written for", tag)
 

@@ -95,3 +95,9 @@ if len(sys.argv) > 4:
             tj[f"{workload}:{kind}:{lev}"] = round(b / frames)
         json.dump(tj, open(tp, "w"), indent=1, sort_keys=True)
         print("traffic ->", tp)
+        if len(sys.argv) > 6:  # argv[6]: pixels per frame -> DRAM bytes per pixel of the whole sequence
+            px = float(sys.argv[6])
+            tot = sum(rows_bytes[:len(order)]) / frames
+            with open(out_md, "a") as f:
+                f.write(f"\nWhole filter sequence: DRAM {tot / 1e6:.1f} MB per frame = {tot / px:.1f} B per level-0 "
+                        f"pixel (read + write, cold caches).\n")
