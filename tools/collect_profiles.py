@@ -73,12 +73,13 @@ def main():
     if os.path.exists(dst("launches.csv")):
         launch_summary(tag, step_us, len(SEQ_C5.split(",")), "config5")
     summ = os.path.join(ROOT, "tools", "ncu_summary.py")
-    if os.path.exists(src("c5_full.ncu-rep")):  # 8 frames, the 64-frame bench's design
-        subprocess.run([sys.executable, summ, src("c5_full.ncu-rep"), dst("ncu_full_config5.md"), "config5", SEQ_C5, "8",
+    rep = lambda n: src(f"{n}.ncu-rep") if os.path.exists(src(f"{n}.ncu-rep")) else src(f"{n}_raw.csv")  # noqa: E731
+    if os.path.exists(rep("c5_full")):  # 8 frames, the 64-frame bench's design
+        subprocess.run([sys.executable, summ, rep("c5_full"), dst("ncu_full_config5.md"), "config5", SEQ_C5, "8",
                         str(1080 * 1920)],
                        check=True, stdout=subprocess.DEVNULL)
-    if os.path.exists(src("c2_full.ncu-rep")):
-        subprocess.run([sys.executable, summ, src("c2_full.ncu-rep"), dst("ncu_full_config2.md"), "config2", SEQ_C2, "1",
+    if os.path.exists(rep("c2_full")):
+        subprocess.run([sys.executable, summ, rep("c2_full"), dst("ncu_full_config2.md"), "config2", SEQ_C2, "1",
                         str(1080 * 1920)],
                        check=True, stdout=subprocess.DEVNULL)
     print("profiles written for", tag)

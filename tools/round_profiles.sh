@@ -30,3 +30,9 @@ python tools/ncu_target.py --workload config2 --iters 1 > gpurun_out/${TAG}_plai
 ncu --set full --import-source on --clock-control none -k regex:"k_apply|k_build|k_fuse|k_collapse" -c 10 \
     -o gpurun_out/${TAG}_c2_full -f python tools/ncu_target.py --workload config2 --iters 1 > gpurun_out/${TAG}_ncu_c2.log 2>&1
 echo "c2 full rc=$?"
+# keep the raw metric pages only (gpurun copies back <= 64 MiB)
+for r in c5_full c2_full; do
+  if [ -f gpurun_out/${TAG}_$r.ncu-rep ]; then
+    ncu -i gpurun_out/${TAG}_$r.ncu-rep --page raw --csv > gpurun_out/${TAG}_${r}_raw.csv 2>/dev/null && rm -f gpurun_out/${TAG}_$r.ncu-rep
+  fi
+done
