@@ -21,27 +21,29 @@
 // compute the same D planes (exact algebra, different rounding order only).
 //
 // k_fuse layout.  CTA = one strip (R coarse rows x 28 coarse columns of one
-// frame) with NW = KL/NC "build" warps and 2 "sum" warps.  Build warp w owns
-// the NC orders [w NC, (w+1) NC) of the plan's order range; lane L holds
+// frame) with one warp per NC orders (NC = 1 for K <= 16: 16 warps).  Warp w
+// owns the NC orders [w NC, (w+1) NC) of the plan's order range; lane L holds
 // coarse column x = 28 cb + L - 2 and fine columns 2x, 2x+1 (reflect-101 per
 // lane at the frame borders).  It streams fine row pairs P_j = (2j, 2j+1),
 // j = o0-2 .. o0+R+1, through its own shared-memory ring (cp.async, PD pairs
-// ahead): the VERTICAL 5-tap with two rolling accumulators per order and
-// column, then the HORIZONTAL 5-tap on the finished coarse row from warp
-// shuffles (k_build's arithmetic, so G_{l+1} and Z_{l+1} are bit-identical to
-// design AB).  Lanes 1..30 hold valid coarse values; with the reflected fine
-// columns / rows those obey the up-sampling border rule (column -1 = x_1,
-// column C = x_{C-1} or x_{C-2}), so the coarse rows o0-1, o0+R and lanes 1, 30
-// are the up-sampling halo.  The last three coarse rows stay in registers,
-// and so do the Z_l values of the last three pairs; once coarse row i+1 is
-// finished the warp forms, for the 4 fine pixels of pair P_i per lane,
-//     V_k = Z_{l,k} - up(Z_{l+1,k})        (the complex Laplacian coefficient)
-// and writes it to a double-buffered shared array V[pair][k][row][col].  The
-// two sum warps (one per fine row of the pair; 2 pixels per lane) evaluate
+// ahead; warp 0 also stages G_l): the VERTICAL 5-tap with two rolling
+// accumulators per order and column, then the HORIZONTAL 5-tap on the
+// finished coarse row from warp shuffles (k_build's arithmetic, so G_{l+1}
+// and Z_{l+1} are bit-identical to design AB).  Lanes 1..30 hold valid coarse
+// values; with the reflected fine columns / rows those obey the up-sampling
+// border rule (column -1 = x_1, column C = x_{C-1} or x_{C-2}), so the coarse
+// rows o0-1, o0+R and lanes 1, 30 are the up-sampling halo.  The last three
+// coarse rows stay in registers, and so do the Z_l values of the last three
+// pairs; once coarse row i+1 is finished the warp forms, for the 4 fine
+// pixels of pair P_i per lane, the Clenshaw coefficient pair of its order
+//     c_k = a_k (Im V_k, -Re V_k),   V_k = Z_{l,k} - up(Z_{l+1,k}),
+// and writes it to the shared array C[pair][k][row][col].  Every 3 pairs (one
+// iteration of the stream loop, unrolled by 3 for the register rotation) the
+// CTA meets at a named barrier and evaluates the batch's order sums
 //     S = sum_k a_k Im(e^{-i k theta} V_k),   theta = w_1 g,
-// with Clenshaw's recurrence over ALL the plan's orders (one sincos per pixel,
-// no cross-warp reduction) and store S into D_l.  Named barriers FULL / EMPTY
-// per V buffer pace the producers and consumers.
+// one pixel per thread, Clenshaw's recurrence over ALL the plan's orders (one
+// sincos per pixel, no cross-warp reduction), stores S into D_l and meets at
+// the barrier again before C is overwritten.
 #include <cstdio>
 #include <cuda_runtime.h>
 #include <stdint.h>
