@@ -591,22 +591,26 @@ struct Build0Warp {
   // Stream the strip: pairs 0 (halo rows) .. R and the final row (even row of
   // pair R+1), PD pairs in flight through the shared-memory ring.
   __device__ __forceinline__ void run(int R) {
-    // pairs 0 .. R+1+PD are read: rows 2(o0-1) .. 2(o0+R+PD)+1
-    rows_in = o0 >= 1 && 2 * (o0 - 1) >= P.fr_lo && 2 * (o0 + R + PD) + 1 <= P.fr_hi;
+    // pairs 0 .. R+1 are read: rows 2(o0-1) .. 2(o0+R)+1 (no copies past the
+    // strip: empty commit groups keep the wait counts uniform)
+    rows_in = o0 >= 1 && 2 * (o0 - 1) >= P.fr_lo && 2 * (o0 + R) + 1 <= P.fr_hi;
     rowp = isrc + (long long)(2 * (o0 - 1)) * ipitch;
 #pragma unroll
-    for (int q = 0; q < PD; ++q) issue_pair(q);
+    for (int q = 0; q < PD; ++q) {
+      if (q <= R + 1) issue_pair(q);
+      else cp_async_commit();
+    }
     cp_async_wait<PD - 1>();
     proc<false, false>(read_pair(0), 0);
-    issue_pair(PD);
+    if (PD <= R + 1) issue_pair(PD); else cp_async_commit();
     cp_async_wait<PD - 1>();
     proc<false, false>(read_pair(1), 0);
-    issue_pair(PD + 1);
+    if (PD + 1 <= R + 1) issue_pair(PD + 1); else cp_async_commit();
 #pragma unroll 1
     for (int p = 2; p <= R; ++p) {
       cp_async_wait<PD - 1>();
       const Pair d = read_pair(p);
-      issue_pair(p + PD);  // beyond the strip: harmless reflected reads
+      if (p + PD <= R + 1) issue_pair(p + PD); else cp_async_commit();
       proc<true, false>(d, o0 + p - 2);
     }
     cp_async_wait<PD - 1>();
