@@ -141,6 +141,22 @@ FLLF_API fllf_status fllf_build_fourier_pyramids(fllf_plan p, const float* d_img
 FLLF_API fllf_status fllf_apply(fllf_plan p, const fllf_apply_args* a, float* d_out,
                        size_t out_pitch_bytes, void* s);
 
+/* n applies in MAPS mode (Sec. III-B: the pyramids do not depend on
+ * the maps, "build once, apply many") with the map pairs (sigma_r_j, m_j),
+ * j = 0..n-1, stacked at map_stride_bytes (0: H * map_pitch_bytes; a multiple
+ * of 16) in d_sigma_r / d_m (each map H x W fp32, map_pitch_bytes per row,
+ * 0 = W * 4; 16-byte aligned rows as fllf_apply(MAPS) needs for its TMA path),
+ * outputs stacked at out_stride_bytes (0: one output = batch x H rows of
+ * out_pitch_bytes) in d_out.  Output j equals fllf_apply(MAPS) with pair j,
+ * bit for bit; the Gaussian pyramids of all n map pairs are built first, one
+ * launch per level for all pairs (the plan keeps n pyramid slots), then the
+ * applies run pair by pair.  Full-frame plans; FLLF_ERR_NOT_BUILT before a
+ * build, FLLF_ERR_INVALID_ARGUMENT for n < 1, strides below one map / output
+ * or row-band plans. */
+FLLF_API fllf_status fllf_apply_maps(fllf_plan p, int n, const float* d_sigma_r, const float* d_m,
+                                     size_t map_pitch_bytes, size_t map_stride_bytes, float* d_out,
+                                     size_t out_pitch_bytes, size_t out_stride_bytes, void* s);
+
 /* As fllf_apply (SCALAR / COEFFS, full-frame plans), but the level-0 result is
  * ADDED to d_out with hardware atomics instead of stored: the combine step of
  * order sharding (linearity of Eq. 4) fused into the apply's

@@ -72,6 +72,8 @@ struct fllf_plan_s {
   size_t ws_bytes = 0;
   void* maps_ws = nullptr;
   size_t maps_ws_bytes = 0;
+  int maps_slots = 0;                           // map-pyramid slots (fllf_apply_maps: one per map pair)
+  long long maps_slot_stride[FLLF_MAX_LEVELS] = {};  // floats between slots, per level
   const char* dbg_out_lo = nullptr;  // debug-bounds builds: the current apply's output range
   const char* dbg_out_hi = nullptr;
   bool built = false;
@@ -574,13 +576,22 @@ fllf_status fllf_build_level(fllf_plan p, const float* d_img, size_t pitch_bytes
   return FLLF_OK;
 }
 
-static fllf_status ensure_maps_ws(fllf_plan p) {
-  if (p->maps_ws) return FLLF_OK;
+// Map-pyramid workspace with `slots` slots per level (slot j: G_l[sigma_j],
+// then G_l[m_j]); lv[l].MS / MM point at slot 0.
+static fllf_status ensure_maps_ws(fllf_plan p, int slots = 1) {
+  if (p->maps_ws && p->maps_slots >= slots) return FLLF_OK;
+  if (p->maps_ws) {
+    cudaError_t e = cudaFree(p->maps_ws);  // (callers are stream-ordered before the next kernels)
+    if (e != cudaSuccess) return cuda_fail(e, "map pyramid cudaFree");
+    p->maps_ws = nullptr;
+    p->maps_slots = 0;
+  }
   size_t off = 0;
   std::vector<size_t> offs(p->nlev);
   for (int l = 1; l < p->nlev; ++l) {
     offs[l] = off;
-    off = align_up(off + 2 * (size_t)p->lv[l].fstride_r * sizeof(float), 256);
+    p->maps_slot_stride[l] = 2 * p->lv[l].fstride_r;
+    off = align_up(off + (size_t)slots * 2 * (size_t)p->lv[l].fstride_r * sizeof(float), 256);
   }
   cudaError_t e = cudaMalloc(&p->maps_ws, off);
   if (e != cudaSuccess) {
@@ -588,6 +599,7 @@ static fllf_status ensure_maps_ws(fllf_plan p) {
     return fail(FLLF_ERR_OUT_OF_MEMORY, "map pyramid cudaMalloc failed");
   }
   p->maps_ws_bytes = off;
+  p->maps_slots = slots;
   char* base = static_cast<char*>(p->maps_ws);
   for (int l = 1; l < p->nlev; ++l) {
     p->lv[l].MS = reinterpret_cast<float*>(base + offs[l]);
@@ -672,8 +684,11 @@ static fllf_status apply_level_impl(fllf_plan p, fllf::ApplyParams& ap, int l, b
 // Apply levels hi down to lo (coarse to fine): fllf_apply (lo = 0, hi = l_max-1),
 // fllf_apply_level (lo = hi = level) and design F's AB levels / level 0
 // (chain_pdl: PDL-linked to the launches before it).
+// maps_prebuilt: MAPS with the map pyramids already in lv[l].MS / MM
+// (fllf_apply_maps builds those of all its map pairs in one launch per level).
 static fllf_status apply_impl(fllf_plan p, const fllf_apply_args* a, float* d_out, size_t out_pitch_bytes, void* s,
-                              int lo, int hi, bool accumulate = false, bool chain_pdl = false) {
+                              int lo, int hi, bool accumulate = false, bool chain_pdl = false,
+                              bool maps_prebuilt = false) {
   if (!p) return fail(FLLF_ERR_BAD_POINTER, "NULL plan");
   if (!p->built) return fail(FLLF_ERR_NOT_BUILT, "fllf_apply before fllf_build_fourier_pyramids");
   long long opitch;
@@ -746,14 +761,14 @@ static fllf_status apply_impl(fllf_plan p, const fllf_apply_args* a, float* d_ou
     if (st != FLLF_OK) return st;
     st = check_image(a->d_m, a->map_pitch_bytes, p->d.W, "apply(MAPS): d_m", &mp2);
     if (st != FLLF_OK) return st;
-    st = ensure_maps_ws(p);
+    if (!maps_prebuilt) st = ensure_maps_ws(p);
     if (st != FLLF_OK) return st;
     ap.smap.p = a->d_sigma_r;
     ap.smap.pitch = mp1;
     ap.mmap.p = a->d_m;
     ap.mmap.pitch = mp2;
     // Gaussian pyramids of the two maps, levels 1 .. l_max-1 (reading R7)
-    for (int l = 0; l + 2 < p->nlev; ++l) {
+    for (int l = 0; l + 2 < p->nlev && !maps_prebuilt; ++l) {
       fllf::BuildParams bp{};
       bp.img.p = a->d_sigma_r;
       bp.img.pitch = mp1;
@@ -801,6 +816,91 @@ fllf_status fllf_apply(fllf_plan p, const fllf_apply_args* a, float* d_out, size
     return fail(FLLF_ERR_INVALID_ARGUMENT,
                 "apply: row-band plans need the per-level calls (halo exchange between levels)");
   return apply_impl(p, a, d_out, out_pitch_bytes, s, 0, p ? p->nlev - 2 : 0);
+}
+
+fllf_status fllf_apply_maps(fllf_plan p, int n, const float* d_sigma_r, const float* d_m, size_t map_pitch_bytes,
+                            size_t map_stride_bytes, float* d_out, size_t out_pitch_bytes, size_t out_stride_bytes,
+                            void* s) {
+  if (!p) return fail(FLLF_ERR_BAD_POINTER, "NULL plan");
+  if (p->band) return fail(FLLF_ERR_INVALID_ARGUMENT, "apply_maps: not for row-band plans");
+  if (!p->built) return fail(FLLF_ERR_NOT_BUILT, "apply_maps before fllf_build_fourier_pyramids");
+  if (n < 1) return fail(FLLF_ERR_INVALID_ARGUMENT, "apply_maps: n >= 1");
+  if (!d_sigma_r || !d_m || !d_out) return fail(FLLF_ERR_BAD_POINTER, "apply_maps: NULL pointer");
+  const size_t mpitch = map_pitch_bytes ? map_pitch_bytes : (size_t)p->d.W * sizeof(float);
+  const size_t opitch = out_pitch_bytes ? out_pitch_bytes : (size_t)p->d.W * sizeof(float);
+  const size_t mstride = map_stride_bytes ? map_stride_bytes : mpitch * p->d.H;
+  const size_t ostride = out_stride_bytes ? out_stride_bytes : opitch * p->d.H * p->d.batch;
+  if ((mstride & 15) || mstride < mpitch * p->d.H)
+    return fail(FLLF_ERR_INVALID_ARGUMENT, "apply_maps: map stride not a multiple of 16 bytes or below one map");
+  if ((ostride & 3) || ostride < opitch * p->d.H * p->d.batch)
+    return fail(FLLF_ERR_INVALID_ARGUMENT, "apply_maps: output stride below one output");
+  long long mp1, mp2;
+  fllf_status st = check_image(d_sigma_r, mpitch, p->d.W, "apply_maps: d_sigma_r", &mp1);
+  if (st != FLLF_OK) return st;
+  st = check_image(d_m, mpitch, p->d.W, "apply_maps: d_m", &mp2);
+  if (st != FLLF_OK) return st;
+  DeviceGuard guard(p->device);
+  cudaStream_t stream = static_cast<cudaStream_t>(s);
+  st = ensure_maps_ws(p, n);
+  if (st != FLLF_OK) return st;
+  p->nrec = 0;  // profiling records of this call: the map builds, then every pair's applies
+  // the map pyramids of all n pairs, one launch per level (blockIdx.z = pair)
+  int launches = 0;
+  for (int l = 0; l + 2 < p->nlev; ++l) {
+    fllf::BuildParams bp{};
+    bp.img.p = d_sigma_r;
+    bp.img.pitch = mp1;
+    bp.img.fstride = (long long)(mstride / sizeof(float));
+    bp.img2.p = d_m;
+    bp.img2.pitch = mp2;
+    bp.img2.fstride = (long long)(mstride / sizeof(float));
+    if (l > 0) bp.src = p->lv[l];
+    bp.dst = p->lv[l + 1];
+    bp.ms_stride_src = l > 0 ? p->maps_slot_stride[l] : 0;
+    bp.ms_stride_dst = p->maps_slot_stride[l + 1];
+    bp.Hf = p->Hs[l];
+    bp.Wf = p->Ws[l];
+    bp.Hc = p->Hs[l + 1];
+    bp.Wc = p->Ws[l + 1];
+    bp.KL = 0;
+    bp.kbase = p->kb;
+    bp.maps = 1;
+    bp.o_begin = 0;
+    bp.o_end = p->Hs[l + 1];
+    bp.fr_lo = 0;
+    bp.fr_hi = p->Hs[l] - 1;
+    bp.invT = (float)(1.0 / p->d.T);
+    bp.dbg_lo = static_cast<const char*>(p->maps_ws);
+    bp.dbg_hi = bp.dbg_lo + p->maps_ws_bytes;
+    cudaError_t e;
+    {
+      ProfScope ps(p, stream, FLLF_K_MAPBUILD, l);
+      e = fllf::launch_build(bp, l, n, stream, false);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "map pyramid kernel launch");
+    ++launches;
+  }
+  // the applies, pair by pair, each reading its slot of the map pyramids
+  fllf::DevLevel saved[FLLF_MAX_LEVELS];
+  for (int l = 1; l < p->nlev; ++l) saved[l] = p->lv[l];
+  for (int j = 0; j < n && st == FLLF_OK; ++j) {
+    for (int l = 1; l < p->nlev; ++l) {
+      p->lv[l].MS = saved[l].MS + j * p->maps_slot_stride[l];
+      p->lv[l].MM = saved[l].MM + j * p->maps_slot_stride[l];
+    }
+    fllf_apply_args a{};
+    a.mode = FLLF_MAPS;
+    a.d_sigma_r = reinterpret_cast<const float*>(reinterpret_cast<const char*>(d_sigma_r) + j * mstride);
+    a.d_m = reinterpret_cast<const float*>(reinterpret_cast<const char*>(d_m) + j * mstride);
+    a.map_pitch_bytes = mpitch;
+    float* out = reinterpret_cast<float*>(reinterpret_cast<char*>(d_out) + j * ostride);
+    p->last_was_apply = false;  // keep the records of the launches before
+    st = apply_impl(p, &a, out, opitch, s, 0, p->nlev - 2, false, false, true);
+    launches += p->last_launches;
+  }
+  for (int l = 1; l < p->nlev; ++l) p->lv[l] = saved[l];
+  p->last_launches = launches;
+  return st;
 }
 
 fllf_status fllf_apply_accumulate(fllf_plan p, const fllf_apply_args* a, float* d_out, size_t out_pitch_bytes,

@@ -54,6 +54,9 @@ struct BuildParams {
   int nchunks;         // complex channel chunks per frame
   int rows_per_strip;  // coarse rows per warp
   int maps;            // 1: build the (sigma, m) map pyramids instead of G/Z
+  // maps: floats between the map-pyramid slots of consecutive map pairs
+  // (blockIdx.z = map index; fllf_apply_maps), at the source / destination level
+  long long ms_stride_src, ms_stride_dst;
   float invT;          // 1/T
   // Row bands (NEXT-1; full frame: o_begin = 0, o_end = Hc, fr_lo = 0,
   // fr_hi = Hf-1).  Rows are GLOBAL level indices everywhere (the plane

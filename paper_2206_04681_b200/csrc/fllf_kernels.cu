@@ -108,16 +108,16 @@ struct BuildWarp {
       rpitch = P.img.pitch;
     } else {
       if (P.maps) {
-        rsrc[0] = P.src.MS;
-        if (NR > 1) rsrc[NR - 1] = P.src.MM;
+        rsrc[0] = P.src.MS + frame * P.ms_stride_src;
+        if (NR > 1) rsrc[NR - 1] = P.src.MM + frame * P.ms_stride_src;
       } else {
         rsrc[0] = P.src.G + frame * P.src.fstride_r;
       }
       rpitch = P.src.pitch;
     }
     if (P.maps) {
-      rdst[0] = P.dst.MS;
-      if (NR > 1) rdst[NR - 1] = P.dst.MM;
+      rdst[0] = P.dst.MS + frame * P.ms_stride_dst;
+      if (NR > 1) rdst[NR - 1] = P.dst.MM + frame * P.ms_stride_dst;
     } else {
       rdst[0] = P.dst.G + frame * P.dst.fstride_r;
     }
@@ -1706,8 +1706,8 @@ cudaError_t launch_build(const BuildParams& p0, int level_src, int batch, cudaSt
   if (p.maps) {
     const int bx = (p.Wc + 29) / 30;
     p.nchunks = 1;
-    p.rows_per_strip = pick_rows(p.o_end - p.o_begin, bx, 1);
-    dim3 grid(bx, (p.o_end - p.o_begin + p.rows_per_strip - 1) / p.rows_per_strip, 1);
+    p.rows_per_strip = pick_rows(p.o_end - p.o_begin, bx, batch);
+    dim3 grid(bx, (p.o_end - p.o_begin + p.rows_per_strip - 1) / p.rows_per_strip, batch);  // z: map pairs
     if (level_src == 0) return launch_ex(k_build<0, 2, true, false>, grid, dim3(32), 0, s, pdl, p);
     return launch_ex(k_build<0, 2, false, false>, grid, dim3(32), 0, s, pdl, p);
   }

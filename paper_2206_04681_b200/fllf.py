@@ -67,6 +67,8 @@ _SIGS = {
     "fllf_build_fourier_pyramids": (ctypes.c_int, [_P, _P, ctypes.c_size_t, _P]),
     "fllf_apply": (ctypes.c_int, [_P, ctypes.POINTER(fllf_apply_args), _P, ctypes.c_size_t, _P]),
     "fllf_apply_accumulate": (ctypes.c_int, [_P, ctypes.POINTER(fllf_apply_args), _P, ctypes.c_size_t, _P]),
+    "fllf_apply_maps": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, ctypes.c_size_t, ctypes.c_size_t, _P,
+                                       ctypes.c_size_t, ctypes.c_size_t, _P]),
     "fllf_ipc_alloc": (ctypes.c_int, [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p), _P]),
     "fllf_ipc_free": (ctypes.c_int, [_P]),
     "fllf_ipc_open": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_void_p)]),
@@ -204,6 +206,27 @@ def fllf_apply(plan, out, mode=FLLF_SCALAR, a_k=None, sigma_map=None, m_map=None
         args.d_sigma_r, args.d_m, args.map_pitch_bytes = sp, mp, spitch
     _check(lib.fllf_apply(plan, ctypes.byref(args), optr, opitch, _stream_handle(stream)))
     del keep
+
+
+def fllf_apply_maps(plan, outs, sigma_maps, m_maps, stream=None) -> None:
+    """n MAPS applies (output j = fllf_apply(MAPS) with map pair j): sigma_maps,
+    m_maps (n, H, W) float32 CUDA tensors with the same layout, outs (n, ..., H, W)
+    with one plan output (batch x H x W) per pair, contiguous per pair."""
+    import torch
+    for t, nm in ((sigma_maps, "sigma_maps"), (m_maps, "m_maps"), (outs, "outs")):
+        if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float32 or t.stride(-1) != 1:
+            raise TypeError(f"{nm} must be a float32 CUDA tensor with unit column stride")
+    if sigma_maps.dim() != 3 or m_maps.shape != sigma_maps.shape or sigma_maps.stride() != m_maps.stride():
+        raise ValueError("sigma_maps and m_maps: (n, H, W) tensors of one layout")
+    n = sigma_maps.shape[0]
+    if outs.shape[0] != n:
+        raise ValueError("outs: one output per map pair")
+    if sigma_maps.stride(1) * sigma_maps.shape[1] > sigma_maps.stride(0) or outs[0].numel() > outs.stride(0) or \
+            not outs[0].is_contiguous():
+        raise ValueError("maps / outputs overlap, or an output is not contiguous")
+    _check(lib.fllf_apply_maps(plan, n, sigma_maps.data_ptr(), m_maps.data_ptr(), sigma_maps.stride(1) * 4,
+                               sigma_maps.stride(0) * 4, outs.data_ptr(), outs.stride(-2) * 4, outs.stride(0) * 4,
+                               _stream_handle(stream)))
 
 
 def fllf_apply_accumulate(plan, out, mode=FLLF_SCALAR, a_k=None, stream=None) -> None:
@@ -559,6 +582,12 @@ class Plan:
     def apply(self, out, **kw):
         self._check_frames(out, "out")
         fllf_apply(self.handle, out, **kw)
+
+    def apply_maps(self, outs, sigma_maps, m_maps, stream=None):
+        """outs[j] = apply(MAPS, sigma_maps[j], m_maps[j]) for every pair j."""
+        for j in range(outs.shape[0]):
+            self._check_frames(outs[j], "outs[j]")
+        fllf_apply_maps(self.handle, outs, sigma_maps, m_maps, stream)
 
     def filter(self, img, out, stream=None):
         self._check_frames(img, "img")
