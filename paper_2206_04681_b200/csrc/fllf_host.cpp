@@ -74,6 +74,17 @@ struct fllf_plan_s {
   size_t maps_ws_bytes = 0;
   int maps_slots = 0;                           // map-pyramid slots (fllf_apply_maps: one per map pair)
   long long maps_slot_stride[FLLF_MAX_LEVELS] = {};  // floats between slots, per level
+  // fllf_apply_maps, map-batched applies: one D plane per pair and level
+  // (mbD_slots planes, fstride_r apart) with their tensor maps; mb_active
+  // while its launches are issued (apply_level_impl / apply_impl read it)
+  void* mbD_ws = nullptr;
+  int mbD_slots = 0;
+  float* mbD[FLLF_MAX_LEVELS] = {};
+  CUtensorMap tmD_mb[FLLF_MAX_LEVELS];
+  bool tmD_mb_ok = false;
+  bool mb_active = false;
+  int mb_n = 0;  // map pairs of the active batched call
+  long long mb_map_fstride = 0;  // floats between the level-0 maps of consecutive pairs
   const char* dbg_out_lo = nullptr;  // debug-bounds builds: the current apply's output range
   const char* dbg_out_hi = nullptr;
   bool built = false;
@@ -470,6 +481,7 @@ fllf_status fllf_destroy(fllf_plan p) {
     cudaDeviceSynchronize();
     if (p->ws) cudaFree(p->ws);
     if (p->maps_ws) cudaFree(p->maps_ws);
+    if (p->mbD_ws) cudaFree(p->mbD_ws);
     if (p->stage_in) cudaFree(p->stage_in);
     if (p->color_ws) cudaFree(p->color_ws);
     if (p->stage_out) cudaFree(p->stage_out);
@@ -628,10 +640,11 @@ static fllf_status apply_level_impl(fllf_plan p, fllf::ApplyParams& ap, int l, b
   ap.coarse = p->lv[l + 1];
   ap.use_tm = p->tm_ok ? 1 : 0;
   ap.use_tm_g = ap.use_tm_d = 0;
+  ap.ms_fstride = p->mb_active && l > 0 ? p->maps_slot_stride[l] : 0;
   if (p->tm_ok) {
     ap.tm_coarse = p->tmc[l + 1];
-    ap.tm_d = p->tmD[l + 1];
-    ap.use_tm_d = 1;
+    ap.tm_d = p->mb_active ? p->tmD_mb[l + 1] : p->tmD[l + 1];
+    ap.use_tm_d = (!p->mb_active || p->tmD_mb_ok) ? 1 : 0;
     if (l > 0) {
       ap.tm_fine = p->tmf[l];
       ap.tm_g = p->tmG[l];
@@ -676,7 +689,7 @@ static fllf_status apply_level_impl(fllf_plan p, fllf::ApplyParams& ap, int l, b
   cudaError_t e;
   {
     ProfScope ps(p, stream, l == 0 ? FLLF_K_APPLY0 : FLLF_K_APPLY, l);
-    e = fllf::launch_apply(ap, l, has_d, maps, p->d.batch, stream, pdl);
+    e = fllf::launch_apply(ap, l, has_d, maps, p->mb_active ? p->mb_n : p->d.batch, stream, pdl);
   }
   return e == cudaSuccess ? FLLF_OK : cuda_fail(e, "apply kernel launch");
 }
@@ -707,6 +720,7 @@ static fllf_status apply_impl(fllf_plan p, const fllf_apply_args* a, float* d_ou
   const double w1 = 2.0 * kPi / T;
 
   fllf::ApplyParams ap{};
+  ap.gz = ap.zz = p->mb_active ? 0 : 1;  // map-batched: tiles of pair j share G, I and Z
   ap.img.p = p->img;
   ap.img.H = p->d.H;
   ap.img.W = p->d.W;
@@ -716,8 +730,8 @@ static fllf_status apply_impl(fllf_plan p, const fllf_apply_args* a, float* d_ou
   ap.accumulate = accumulate ? 1 : 0;
   // debug-bounds builds: level 0 writes the caller's rows, levels >= 1 the workspace
   p->dbg_out_lo = reinterpret_cast<const char*>(d_out);
-  p->dbg_out_hi = p->dbg_out_lo + ((size_t)(p->d.batch - 1) * p->d.H + (p->d.row_end - p->d.row_begin)) *
-                                      (size_t)opitch * sizeof(float);
+  p->dbg_out_hi = p->dbg_out_lo + ((size_t)((p->mb_active ? p->mb_n : p->d.batch) - 1) * p->d.H +
+                                     (p->d.row_end - p->d.row_begin)) * (size_t)opitch * sizeof(float);
   ap.out_pitch = opitch;
   ap.out_fstride = opitch * p->d.H;
   ap.KL = p->KL;
@@ -767,6 +781,7 @@ static fllf_status apply_impl(fllf_plan p, const fllf_apply_args* a, float* d_ou
     ap.smap.pitch = mp1;
     ap.mmap.p = a->d_m;
     ap.mmap.pitch = mp2;
+    ap.smap.fstride = ap.mmap.fstride = p->mb_active ? p->mb_map_fstride : 0;
     // Gaussian pyramids of the two maps, levels 1 .. l_max-1 (reading R7)
     for (int l = 0; l + 2 < p->nlev && !maps_prebuilt; ++l) {
       fllf::BuildParams bp{};
@@ -879,6 +894,69 @@ fllf_status fllf_apply_maps(fllf_plan p, int n, const float* d_sigma_r, const fl
     }
     if (e != cudaSuccess) return cuda_fail(e, "map pyramid kernel launch");
     ++launches;
+  }
+  // map-batched applies: one launch per level for all n pairs (tile frame
+  // index = pair; G, I and Z shared, D / map planes / output per pair) --
+  // single-frame plans, 16-byte aligned map rows (the TMA-staged MAPS path)
+  const bool aligned = ((reinterpret_cast<uintptr_t>(d_sigma_r) | reinterpret_cast<uintptr_t>(d_m)) & 15) == 0 &&
+                       (mp1 & 3) == 0 && mp1 == mp2 && (p->d.W & 3) == 0 && ((mstride / 4) & 3) == 0;
+  static const bool mb_off = [] {  // FLLF_APPLY_MAPS_PER_PAIR=1: applies pair by pair (A/B)
+    const char* e = std::getenv("FLLF_APPLY_MAPS_PER_PAIR");
+    return e && e[0] == '1';
+  }();
+  if (!mb_off && p->d.batch == 1 && aligned && ostride == opitch * p->d.H) {
+    if (p->mbD_slots < n) {  // per-pair D planes of every level >= 1
+      if (p->mbD_ws) cudaFree(p->mbD_ws);
+      p->mbD_ws = nullptr;
+      p->mbD_slots = 0;
+      // guard bands: the tile-header copies of D rows start 4 columns left of
+      // a row and may run past its end (as inside the plan's workspace)
+      size_t off = 256;
+      std::vector<size_t> offs(p->nlev);
+      for (int l = 1; l < p->nlev; ++l) {
+        offs[l] = off;
+        off = align_up(off + (size_t)n * p->lv[l].fstride_r * sizeof(float) + 256, 256);
+      }
+      off += 4096;
+      cudaError_t e = cudaMalloc(&p->mbD_ws, off);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(FLLF_ERR_OUT_OF_MEMORY, "apply_maps: D planes cudaMalloc failed");
+      }
+      e = cudaMemset(p->mbD_ws, 0, off);
+      if (e != cudaSuccess) return cuda_fail(e, "apply_maps: D planes memset");
+      p->mbD_slots = n;
+      bool ok = p->tm_ok;
+      for (int l = 1; l < p->nlev; ++l) {
+        p->mbD[l] = reinterpret_cast<float*>(static_cast<char*>(p->mbD_ws) + offs[l]);
+        if (ok)
+          ok = encode_real_map(&p->tmD_mb[l], p->mbD[l], p->lv[l].W, p->lv[l].H, n, p->lv[l].pitch,
+                               p->lv[l].fstride_r, 68, 6);
+      }
+      p->tmD_mb_ok = ok;
+    }
+    fllf::DevLevel saved[FLLF_MAX_LEVELS];
+    for (int l = 1; l < p->nlev; ++l) {
+      saved[l] = p->lv[l];
+      p->lv[l].D = p->mbD[l];
+    }
+    p->mb_active = true;
+    p->mb_n = n;
+    p->mb_map_fstride = (long long)(mstride / sizeof(float));
+    fllf_apply_args a{};
+    a.mode = FLLF_MAPS;
+    a.d_sigma_r = d_sigma_r;
+    a.d_m = d_m;
+    a.map_pitch_bytes = mpitch;
+    p->last_was_apply = false;
+    st = apply_impl(p, &a, d_out, opitch, s, 0, p->nlev - 2, false, false, true);
+    launches += p->last_launches;
+    p->mb_active = false;
+    p->mb_n = 0;
+    p->mb_map_fstride = 0;
+    for (int l = 1; l < p->nlev; ++l) p->lv[l] = saved[l];
+    p->last_launches = launches;
+    return st;
   }
   // the applies, pair by pair, each reading its slot of the map pyramids
   fllf::DevLevel saved[FLLF_MAX_LEVELS];

@@ -115,6 +115,13 @@ struct ApplyParams {
   int r_begin, r_end;
   int cr_lo, cr_hi, fr_lo, fr_hi;
   int accumulate;      // level 0: atomically add the output into out (fllf_apply_accumulate)
+  // Frame index of a tile (T.frame) for the G / image planes (gz) and the Z
+  // planes (zz): 1 = per frame; 0 = shared -- MAPS over a batch of map pairs
+  // (fllf_apply_maps), where T.frame is the pair and only D, the map planes
+  // (ms_fstride floats apart at the fine level; smap / mmap .fstride at level
+  // 0) and the output differ between tiles of different pairs.
+  int gz, zz;
+  long long ms_fstride;
   const char* dbg_lo;  // FLLF_DEBUG_BOUNDS builds: every global store must land in [dbg_lo, dbg_hi)
   const char* dbg_hi;
 };

@@ -1190,7 +1190,7 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0, MAPS>()) k_apply_cl
       if (tmg) {
         if (elect_one()) {
           mbar_arrive_expect_tx(&gfull[hb], 8 * HDR_G_ROW);
-          tma_load_3d(hdr, &P.tm_g, 120 * T.jb, 2 * T.r0, T.frame, &gfull[hb]);
+          tma_load_3d(hdr, &P.tm_g, 120 * T.jb, 2 * T.r0, T.frame * P.gz, &gfull[hb]);
         }
         __syncwarp();
       } else if (tma_g) {
@@ -1198,11 +1198,11 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0, MAPS>()) k_apply_cl
         long long gp;
         int wlim;
         if (LEVEL0) {
-          gb = P.img.p + T.frame * P.img.fstride;
+          gb = P.img.p + T.frame * P.gz * P.img.fstride;
           gp = P.img.pitch;
           wlim = P.Wf;
         } else {
-          gb = P.fine.G + T.frame * P.fine.fstride_r;
+          gb = P.fine.G + T.frame * P.gz * P.fine.fstride_r;
           gp = P.fine.pitch;
           wlim = P.fine.pitch;
         }
@@ -1222,13 +1222,13 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0, MAPS>()) k_apply_cl
         long long mp;
         int wlim;
         if (LEVEL0) {
-          sb = P.smap.p;
-          mb = P.mmap.p;
+          sb = P.smap.p + T.frame * P.smap.fstride;
+          mb = P.mmap.p + T.frame * P.mmap.fstride;
           mp = P.smap.pitch;
           wlim = P.Wf;
         } else {
-          sb = P.fine.MS;
-          mb = P.fine.MM;
+          sb = P.fine.MS + T.frame * P.ms_fstride;
+          mb = P.fine.MM + T.frame * P.ms_fstride;
           mp = P.fine.pitch;
           wlim = P.fine.pitch;
         }
@@ -1244,11 +1244,12 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0, MAPS>()) k_apply_cl
         }
         __syncwarp();
       }
-      const float2* zc0 = P.coarse.Z + T.frame * P.coarse.fstride_z + (60 * T.jb - 2);
+      const int zfr = T.frame * P.zz;
+      const float2* zc0 = P.coarse.Z + zfr * P.coarse.fstride_z + (60 * T.jb - 2);
       int crow[6];
 #pragma unroll
       for (int q = 0; q < 6; ++q) crow[q] = min(max(upmap(T.r0 - 1 + q, P.Hc, P.Hf), P.cr_lo), P.cr_hi);
-      const float2* zf0 = LEVEL0 ? nullptr : P.fine.Z + T.frame * P.fine.fstride_z + (120 * T.jb - 4);
+      const float2* zf0 = LEVEL0 ? nullptr : P.fine.Z + zfr * P.fine.fstride_z + (120 * T.jb - 4);
       // interior tiles: the 6 coarse (8 fine) rows are contiguous -> one tensor copy per order
       const bool tmc = P.use_tm && T.r0 >= 1 && T.r0 - 1 >= P.cr_lo && T.r0 + 4 <= min(P.Hc - 1, P.cr_hi);
       const bool tmf = !LEVEL0 && P.use_tm && 2 * T.r0 + 7 <= min(P.Hf - 1, P.fr_hi);
@@ -1265,7 +1266,7 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0, MAPS>()) k_apply_cl
             if (h < no) {
               unsigned char* so = st + h * OBYTES;
               if (tmc) {
-                tma_load_3d(so, &P.tm_coarse, xc, T.r0 - 1, T.frame * KL + i - h, &full[s]);
+                tma_load_3d(so, &P.tm_coarse, xc, T.r0 - 1, zfr * KL + i - h, &full[s]);
               } else {
                 const float2* zc = zc0 + (long long)(i - h) * P.coarse.kstride_z;
 #pragma unroll
@@ -1274,7 +1275,7 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0, MAPS>()) k_apply_cl
               }
               if (!LEVEL0) {
                 if (tmf) {
-                  tma_load_3d(so + FOFF, &P.tm_fine, xf, 2 * T.r0, T.frame * KL + i - h, &full[s]);
+                  tma_load_3d(so + FOFF, &P.tm_fine, xf, 2 * T.r0, zfr * KL + i - h, &full[s]);
                 } else {
                   const float2* zf = zf0 + (long long)(i - h) * P.fine.kstride_z;
 #pragma unroll
@@ -1345,7 +1346,7 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0, MAPS>()) k_apply_cl
     } else {  // caller image not TMA-compatible: direct loads (level 0 only)
       const int rr = min(r, P.Hc - 1);
       const int xf0 = 4 * j;
-      const float* base = P.img.p + T.frame * P.img.fstride;
+      const float* base = P.img.p + T.frame * P.gz * P.img.fstride;
 #pragma unroll
       for (int tt = 0; tt < 2; ++tt) {
         const float* rp = base + (long long)min(2 * rr + tt, P.fr_hi) * P.img.pitch;
