@@ -107,19 +107,33 @@ __device__ __forceinline__ void sts2(uint32_t a, float2 v) {
   asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
 }
 
+// Order-sum hand-over buffers: 1 = one buffer and two CTA barriers per batch
+// (default); 2 = double-buffered C / Gb with mbarriers (warps run one batch
+// apart: a warp streams batch b while the order sums of batch b-1 wait only
+// for the last warp's coefficients of b-1).  Measured at config 5: level 1
+// 1.44-1.51 ms with 2 vs 1.38-1.41 ms with 1, so the
+// barrier coupling is not what limits this kernel; kept for A/B.
+#ifndef FLLF_FUSE_NBUF
+#define FLLF_FUSE_NBUF 1
+#endif
+constexpr int FUSE_NBUF = FLLF_FUSE_NBUF;
+
 // Shared-memory layout of one CTA (bytes), NB = fuse_nb(warps):
-//   C    [NB pairs][KL orders][2 fine rows][64 fine columns] float2   (NB x 1024 KL)
-//   Gb   [NB pairs][2 fine rows][64 fine columns] float                 (NB x 512)
+//   C    [NBUF][NB pairs][KL orders][2 fine rows][64 fine columns] float2   (NBUF x NB x 1024 KL)
+//   Gb   [NBUF][NB pairs][2 fine rows][64 fine columns] float                 (NBUF x NB x 512)
 //   ring of warp 0:  DEPTH slots x (G 512 + Z 1024 NC)
 //   ring of warp w:  DEPTH slots x Z 1024 NC
 template <int NC, int PD>
 struct FuseLayout {
+  static constexpr int NBUF = NC == 1 ? FUSE_NBUF : 1;  // (two orders per warp: K > 16, shared memory)
   static constexpr int DEPTH = PD + 1;
   static constexpr int ZSLOT = NC * 1024;  // NC orders x 2 rows x 32 lanes x float4
   static constexpr int G0SLOT = 512 + ZSLOT;
-  __host__ __device__ static int g_off(int KL) { return fuse_nb(KL / NC) * KL * 1024; }
+  __host__ __device__ static int c_buf(int KL) { return fuse_nb(KL / NC) * KL * 1024; }
+  __host__ __device__ static int g_buf(int KL) { return fuse_nb(KL / NC) * 512; }
+  __host__ __device__ static int g_off(int KL) { return NBUF * c_buf(KL); }
   __host__ __device__ static int ring_off(int KL, int w) {
-    return g_off(KL) + fuse_nb(KL / NC) * 512 + (w == 0 ? 0 : DEPTH * G0SLOT + (w - 1) * DEPTH * ZSLOT);
+    return g_off(KL) + NBUF * g_buf(KL) + (w == 0 ? 0 : DEPTH * G0SLOT + (w - 1) * DEPTH * ZSLOT);
   }
   __host__ __device__ static int smem(int KL) { return ring_off(KL, KL / NC); }
 };
@@ -153,12 +167,14 @@ struct FuseWarp {
   int cb_;
   uint32_t sbase_;
   float* dbase;         // D_l of the frame
+  uint32_t bars;        // mbarriers (NBUF = 2): full[0], full[1], empty[0], empty[1]
+  uint32_t cbo, gbo;    // C / Gb offsets of the buffer being written
   float2 Pc[NC][2], Ac[NC][2];
   float2 Pr, Ar;
 
   __device__ __forceinline__ FuseWarp(const FuseParams& P_, int cb, int o0_, int R_, int frame, int nw_,
-                                      int warp_, uint32_t smem)
-      : P(P_), o0(o0_), R(R_), warp(warp_), nw(nw_) {
+                                      int warp_, uint32_t smem, uint32_t bars_)
+      : P(P_), o0(o0_), R(R_), warp(warp_), nw(nw_), bars(bars_) {
     lane = threadIdx.x & 31;
     nb = fuse_nb(nw);
     Hf = P.Hf;
@@ -193,6 +209,7 @@ struct FuseWarp {
     cb_ = cb;
     sbase_ = smem;
     dbase = P.src.D + frame * P.src.fstride_r;
+    cbo = gbo = 0;
   }
 
   // copies of the next pair (fine rows 2 jn, 2 jn + 1) into the next ring slot
@@ -310,7 +327,7 @@ struct FuseWarp {
   __device__ __forceinline__ void coef(const float2 (&Cm)[NC], const float2 (&C0)[NC], const float2 (&Cp)[NC],
                                        const float4 (&ze)[NC], const float4 (&zo)[NC], const float4& gg, int n,
                                        int& q) {
-    const uint32_t cb = crow + q * (kl() * 1024);
+    const uint32_t cb = crow + cbo + q * (kl() * 1024);
 #pragma unroll
     for (int i = 0; i < NC; ++i) {
       // vertical up-sampling (unscaled): even fine row x_{i-1} + 6 x_i + x_{i+1}, odd x_i + x_{i+1}
@@ -326,7 +343,7 @@ struct FuseWarp {
       sts4(cb + i * 1024 + 512, cat4(c2, c3));
     }
     if (DO_G) {  // g of the pair for the order sums
-      const uint32_t gb = gbrow + q * 512;
+      const uint32_t gb = gbrow + gbo + q * 512;
       sts2(gb, lo2(gg));
       sts2(gb + 256, hi2(gg));
     }
@@ -341,21 +358,31 @@ struct FuseWarp {
   // Clenshaw's recurrence (descending k: b_k = c_k + 2 cos theta b_{k+1} - b_{k+2};
   // see k_apply_cl), stored into D_l.  Between two CTA barriers: C / Gb are
   // complete before, consumed after.
-  __device__ __forceinline__ void order_sum(int n0, int cnt) {
-    bar_sync_id(FUSE_BAR, nw * 32);
+  // Batch bt (own pairs 3 bt ..) in buffer bt % NBUF.  NBUF = 2: wait until
+  // every warp has written its coefficients (full), release the buffer
+  // after reading it (empty); the pixel slots rotate by 4 warps per batch so
+  // the idle quarter (384 pixels, 512 threads) moves around.  NBUF = 1: two
+  // CTA barriers.
+  __device__ __forceinline__ void order_sum(int bt, int cnt) {
+    const int n0 = FUSE_NB * bt;
+    const int ub = L::NBUF == 2 ? (bt & 1) : 0;
+    if (L::NBUF == 2) mbar_wait_u32(bars + 8 * ub, (bt >> 1) & 1);
+    else bar_sync_id(FUSE_BAR, nw * 32);
     if (!(P.exp & 1)) {
       const int KL = kl();
-      const int goff = L::g_off(KL);
+      const uint32_t cbase = sbase_ + ub * L::c_buf(KL);
+      const int goff = L::g_off(KL) + ub * L::g_buf(KL);
       const int row0 = 2 * (o0 + n0);
+      const int slot = L::NBUF == 2 ? (warp + 4 * bt) % nw : warp;
 #pragma unroll 1
-      for (int p = warp * 32 + lane; p < cnt * 128; p += nw * 32) {
+      for (int p = slot * 32 + lane; p < cnt * 128; p += nw * 32) {
         const int q = p >> 7, r = (p >> 6) & 1, f = p & 63;
         const float g = lds1(sbase_ + goff + ((q * 2 + r) * 64 + f) * 4);
         float sn, c1;
         sincos_turns(g, P.invT, &sn, &c1);
         const float2 tc = bc(2.f * c1);
         float2 b1 = make_float2(0.f, 0.f), b2 = b1;
-        uint32_t a = sbase_ + ((q * KL + KL - 1) * 2 + r) * 512 + f * 8;
+        uint32_t a = cbase + ((q * KL + KL - 1) * 2 + r) * 512 + f * 8;
         int k = KL;
 #pragma unroll(KT > 0 ? 8 : 1)
         for (; k >= 4; k -= 4, a -= 4096) {
@@ -390,7 +417,21 @@ struct FuseWarp {
         }
       }
     }
-    bar_sync_id(FUSE_BAR, nw * 32);
+    if (L::NBUF == 2) mbar_arrive_u32(bars + 16 + 8 * ub);
+    else bar_sync_id(FUSE_BAR, nw * 32);
+  }
+
+  // NBUF = 2: before the first coefficients of batch bt, wait until the order
+  // sums of batch bt-2 (same buffer) have read it; after the last, publish.
+  __device__ __forceinline__ void begin_batch(int bt) {
+    if (L::NBUF != 2) return;
+    const int ub = bt & 1;
+    if (bt >= 2) mbar_wait_u32(bars + 16 + 8 * ub, ((bt >> 1) - 1) & 1);
+    cbo = ub * L::c_buf(kl());
+    gbo = ub * L::g_buf(kl());
+  }
+  __device__ __forceinline__ void end_batch(int bt) {
+    if (L::NBUF == 2) mbar_arrive_u32(bars + 8 * (bt & 1));
   }
 
   // One step t (pair P_{o0-2+t}): Wm, W0 = coarse rows j-3, j-2; Wn <- row
@@ -453,19 +494,27 @@ struct FuseWarp {
     step<false, false, true, false>(1, np, FUSE_PH1);
     step<true, false, true, false>(2, np, FUSE_PH2);
     step<true, true, true, false>(3, np, FUSE_PH0);
-    int t = 4;
+    int t = 4, bt = 0;
 #pragma unroll 1
-    for (; t + 2 <= R + 2; t += 3) {  // one batch (own pairs t-4 .. t-2) per iteration
+    for (; t + 2 <= R + 2; t += 3, ++bt) {  // one batch bt (own pairs t-4 .. t-2) per iteration
       q = 0;
+      begin_batch(bt);
       step<true, true, true, true>(t, np, FUSE_PH1);
       step<true, true, true, true>(t + 1, np, FUSE_PH2);
       step<true, true, true, true>(t + 2, np, FUSE_PH0);
-      order_sum(t - 4, FUSE_NB);
+      end_batch(bt);
+      // NBUF = 2: the order sums run one batch behind the coefficients
+      if (L::NBUF == 2) {
+        if (bt > 0) order_sum(bt - 1, FUSE_NB);
+      } else {
+        order_sum(bt, FUSE_NB);
+      }
     }
     // 0..2 steady steps remain (phase 1 first), then the last step t = R+3:
     // the last (partial) batch
     const int rem = R + 3 - t;
     q = 0;
+    begin_batch(bt);
     if (rem == 0) {
       step<true, false, false, true>(t, np, FUSE_PH1);
     } else if (rem == 1) {
@@ -476,7 +525,9 @@ struct FuseWarp {
       step<true, true, true, true>(t + 1, np, FUSE_PH2);
       step<true, false, false, true>(t + 2, np, FUSE_PH0);
     }
-    order_sum(t - 4, rem + 1);
+    end_batch(bt);
+    if (L::NBUF == 2 && bt > 0) order_sum(bt - 1, FUSE_NB);
+    order_sum(bt, rem + 1);
 #undef FUSE_PH0
 #undef FUSE_PH1
 #undef FUSE_PH2
@@ -486,12 +537,12 @@ struct FuseWarp {
 
 template <int NC, int PD, bool EDGE, bool ROWS_IN, int KT>
 __device__ __forceinline__ void fuse_run(const FuseParams& P, int cb, int o0, int R, int frame, int nw, int warp,
-                                         uint32_t sbase) {
+                                         uint32_t sbase, uint32_t bars) {
   if (warp == 0) {
-    FuseWarp<NC, PD, EDGE, true, ROWS_IN, KT> w(P, cb, o0, R, frame, nw, warp, sbase);
+    FuseWarp<NC, PD, EDGE, true, ROWS_IN, KT> w(P, cb, o0, R, frame, nw, warp, sbase, bars);
     w.run();
   } else {
-    FuseWarp<NC, PD, EDGE, false, ROWS_IN, KT> w(P, cb, o0, R, frame, nw, warp, sbase);
+    FuseWarp<NC, PD, EDGE, false, ROWS_IN, KT> w(P, cb, o0, R, frame, nw, warp, sbase, bars);
     w.run();
   }
 }
@@ -501,9 +552,18 @@ __device__ __forceinline__ void fuse_run(const FuseParams& P, int cb, int o0, in
 template <int NC, int PD, int KT = 0>
 __global__ void __launch_bounds__(FUSE_MAX_WARPS * 32, 1) k_fuse(const __grid_constant__ FuseParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bar[4];  // NBUF = 2: full[2], empty[2] of the order-sum buffers
+  if (FuseLayout<NC, PD>::NBUF == 2) {
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) mbar_init(&bar[i], blockDim.x);
+    }
+    __syncthreads();
+  }
   pdl_wait();     // level l (G_l, Z_l) is complete
   pdl_trigger();  // let the next level's kernel get scheduled
   const uint32_t sbase = smem_u32(smem);
+  const uint32_t bars = smem_u32(bar);
   const int cb = blockIdx.x;
   const int o0 = blockIdx.y * P.rows_per_strip;
   const int R = min(P.rows_per_strip, P.Hc - o0);
@@ -515,11 +575,11 @@ __global__ void __launch_bounds__(FUSE_MAX_WARPS * 32, 1) k_fuse(const __grid_co
   // pairs o0-2 .. o0+R+1 inside the frame: no row reflection
   const bool rows_in = o0 >= 2 && 2 * (o0 + R + 1) + 1 < P.Hf;
   if (interior) {
-    if (rows_in) fuse_run<NC, PD, false, true, KT>(P, cb, o0, R, frame, nw, warp, sbase);
-    else fuse_run<NC, PD, false, false, KT>(P, cb, o0, R, frame, nw, warp, sbase);
+    if (rows_in) fuse_run<NC, PD, false, true, KT>(P, cb, o0, R, frame, nw, warp, sbase, bars);
+    else fuse_run<NC, PD, false, false, KT>(P, cb, o0, R, frame, nw, warp, sbase, bars);
   } else {
-    if (rows_in) fuse_run<NC, PD, true, true, KT>(P, cb, o0, R, frame, nw, warp, sbase);
-    else fuse_run<NC, PD, true, false, KT>(P, cb, o0, R, frame, nw, warp, sbase);
+    if (rows_in) fuse_run<NC, PD, true, true, KT>(P, cb, o0, R, frame, nw, warp, sbase, bars);
+    else fuse_run<NC, PD, true, false, KT>(P, cb, o0, R, frame, nw, warp, sbase, bars);
   }
 }
 
@@ -587,7 +647,7 @@ __global__ void __launch_bounds__(128) k_collapse(const CollapseParams P) {
   }
 }
 
-constexpr int kFuseSmemMax = 227 * 1024;
+constexpr int kFuseSmemMax = 227 * 1024 - 64;  // (static shared: the kernel's mbarriers)
 // ring depth (pairs ahead): 4 with one order per warp, 2 with two (shared memory)
 #ifndef FLLF_FUSE_PD1
 #define FLLF_FUSE_PD1 6

@@ -161,13 +161,14 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
-// Z planes of one level as a 3-D fp32 tensor: (2 * zpitch floats) x H rows x
-// (batch * KL) planes; box (bx floats, by rows, 1 plane).
-bool encode_z_map(CUtensorMap* m, const fllf::DevLevel& L, int planes, unsigned bx, unsigned by) {
+// Z planes of one level as a 3-D fp32 tensor: (2 * zpitch floats) x the
+// stored rows lo .. lo + rows - 1 x (batch * KL) planes; box (bx floats, by
+// rows, 1 plane).  Row coordinates are relative to row lo.
+bool encode_z_map(CUtensorMap* m, const fllf::DevLevel& L, int lo, int rows, int planes, unsigned bx, unsigned by) {
   auto enc = tensor_map_encoder();
   if (!enc) return false;
-  void* base = const_cast<float2*>(L.Z - fllf::ZHALO);
-  const cuuint64_t dims[3] = {(cuuint64_t)(2 * L.zpitch), (cuuint64_t)L.H, (cuuint64_t)planes};
+  void* base = const_cast<float2*>(L.Z - fllf::ZHALO + (long long)lo * L.zpitch);
+  const cuuint64_t dims[3] = {(cuuint64_t)(2 * L.zpitch), (cuuint64_t)rows, (cuuint64_t)planes};
   const cuuint64_t strides[2] = {(cuuint64_t)L.zpitch * 8, (cuuint64_t)L.kstride_z * 8};
   const cuuint32_t box[3] = {bx, by, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
@@ -454,9 +455,12 @@ fllf_status fllf_plan_create_ex(const fllf_plan_desc* din, fllf_plan* out) {
     bool ok = true;
     for (int l = 1; l < d.levels && ok; ++l) {
       const fllf::DevLevel& L = p->lv[l];
-      ok = encode_z_map(&p->tmc[l], L, (int)B * p->KL, 128, 6) && encode_z_map(&p->tmf[l], L, (int)B * p->KL, 256, 8) &&
-           encode_real_map(&p->tmG[l], L.G, L.W, L.H, (int)B, L.pitch, L.fstride_r, 120, 8) &&
-           encode_real_map(&p->tmD[l], L.D, L.W, L.H, (int)B, L.pitch, L.fstride_r, 68, 6);
+      // maps over the stored rows al .. ah only (kernels subtract cr_lo / fr_lo)
+      const int lo = p->al[l], rows = p->ah[l] - p->al[l] + 1;
+      ok = encode_z_map(&p->tmc[l], L, lo, rows, (int)B * p->KL, 128, 6) &&
+           encode_z_map(&p->tmf[l], L, lo, rows, (int)B * p->KL, 256, 8) &&
+           encode_real_map(&p->tmG[l], L.G + (long long)lo * L.pitch, L.W, rows, (int)B, L.pitch, L.fstride_r, 120, 8) &&
+           encode_real_map(&p->tmD[l], L.D + (long long)lo * L.pitch, L.W, rows, (int)B, L.pitch, L.fstride_r, 68, 6);
     }
     const char* nt = std::getenv("FLLF_NO_TENSOR_TMA");
     p->tm_ok = ok && !(nt && nt[0] == '1');
@@ -651,8 +655,9 @@ static fllf_status apply_level_impl(fllf_plan p, fllf::ApplyParams& ap, int l, b
       ap.use_tm_g = 1;
     } else {
       if (p->tmI_ptr != p->img || p->tmI_pitch != p->img_pitch) {
-        p->tmI_ok = encode_real_map(&p->tmI, p->img, p->d.W, p->d.H, p->d.batch, p->img_pitch,
-                                    p->img_pitch * p->d.H, 120, 8);
+        // the rows the plan reads (al[0] .. ah[0]; a band's caller may hold only those)
+        p->tmI_ok = encode_real_map(&p->tmI, p->img + (long long)p->al[0] * p->img_pitch, p->d.W,
+                                    p->ah[0] - p->al[0] + 1, p->d.batch, p->img_pitch, p->img_pitch * p->d.H, 120, 8);
         p->tmI_ptr = p->img;
         p->tmI_pitch = p->img_pitch;
       }

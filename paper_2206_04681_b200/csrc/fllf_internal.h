@@ -74,7 +74,11 @@ struct ApplyParams {
   // TMA tensor maps (3-D: float columns x rows x (frame, order) planes) of the
   // coarse level's Z planes (box 128 floats x 6 rows) and the fine level's
   // (box 256 x 8): one tensor copy per order stage for interior tiles
-  // (k_apply_cl); use_tm = 0 -> per-row bulk copies only.
+  // (k_apply_cl); use_tm = 0 -> per-row bulk copies only.  Every map covers
+  // only the rows its level stores (row-band plans: al .. ah; the image: the
+  // rows the band reads), so its row coordinate is the global row minus
+  // cr_lo (coarse level: tm_coarse, tm_d) or fr_lo (fine level / image:
+  // tm_fine, tm_g) -- no map addresses memory outside its allocation.
   CUtensorMap tm_coarse;
   CUtensorMap tm_fine;
   CUtensorMap tm_g;    // g rows of the tile header: I (level 0) or G_l, box 120 floats x 8 rows

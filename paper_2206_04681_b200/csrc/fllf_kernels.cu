@@ -501,6 +501,9 @@ struct Build0Warp {
   }
 
   // horizontal [1,4,6,4,1] + decimation of a finished row (complex), a = col 2x, b = 2x+1
+  // (shuffling a partial sum of the left neighbour's taps, as hfilt_c does,
+  // saves 2 of 6 shuffles but measured 5 % slower here: the shuffles wait for
+  // the FFMA2 that forms it)
   __device__ __forceinline__ static float2 hsum_c(float2 a, float2 b) {
     const float2 La = shfl_up2(a), Lb = shfl_up2(b), Ra = shfl_down2(a);
     return pfma(bc(6.f), a, pfma(bc(4.f), padd(b, Lb), padd(La, Ra)));
@@ -1190,7 +1193,7 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0, MAPS>()) k_apply_cl
       if (tmg) {
         if (elect_one()) {
           mbar_arrive_expect_tx(&gfull[hb], 8 * HDR_G_ROW);
-          tma_load_3d(hdr, &P.tm_g, 120 * T.jb, 2 * T.r0, T.frame * P.gz, &gfull[hb]);
+          tma_load_3d(hdr, &P.tm_g, 120 * T.jb, 2 * T.r0 - P.fr_lo, T.frame * P.gz, &gfull[hb]);
         }
         __syncwarp();
       } else if (tma_g) {
@@ -1266,7 +1269,7 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0, MAPS>()) k_apply_cl
             if (h < no) {
               unsigned char* so = st + h * OBYTES;
               if (tmc) {
-                tma_load_3d(so, &P.tm_coarse, xc, T.r0 - 1, zfr * KL + i - h, &full[s]);
+                tma_load_3d(so, &P.tm_coarse, xc, T.r0 - 1 - P.cr_lo, zfr * KL + i - h, &full[s]);
               } else {
                 const float2* zc = zc0 + (long long)(i - h) * P.coarse.kstride_z;
 #pragma unroll
@@ -1275,7 +1278,7 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0, MAPS>()) k_apply_cl
               }
               if (!LEVEL0) {
                 if (tmf) {
-                  tma_load_3d(so + FOFF, &P.tm_fine, xf, 2 * T.r0, zfr * KL + i - h, &full[s]);
+                  tma_load_3d(so + FOFF, &P.tm_fine, xf, 2 * T.r0 - P.fr_lo, zfr * KL + i - h, &full[s]);
                 } else {
                   const float2* zf = zf0 + (long long)(i - h) * P.fine.kstride_z;
 #pragma unroll
@@ -1303,7 +1306,7 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0, MAPS>()) k_apply_cl
         if (elect_one()) {
           mbar_arrive_expect_tx(&dfull[hb], 6 * HDR_D_ROW);
           if (P.use_tm_d && tmc) {
-            tma_load_3d(hdr + HDR_D_OFF, &P.tm_d, 60 * T.jb - 4, T.r0 - 1, T.frame, &dfull[hb]);
+            tma_load_3d(hdr + HDR_D_OFF, &P.tm_d, 60 * T.jb - 4, T.r0 - 1 - P.cr_lo, T.frame, &dfull[hb]);
           } else {
 #pragma unroll
             for (int q = 0; q < 6; ++q)
