@@ -117,6 +117,12 @@ __device__ __forceinline__ void sts2(uint32_t a, float2 v) {
 #define FLLF_FUSE_NBUF 1
 #endif
 constexpr int FUSE_NBUF = FLLF_FUSE_NBUF;
+// read each ring pair into registers one step ahead (the cp.async wait is a
+// compiler fence).  Off: with the Z_l delay line of 3 pairs already in
+// registers the extra pair spills (92-184 bytes at 128 registers).
+#ifndef FLLF_FUSE_PIPE
+#define FLLF_FUSE_PIPE 0
+#endif
 
 // Shared-memory layout of one CTA (bytes), NB = fuse_nb(warps):
 //   C    [NBUF][NB pairs][KL orders][2 fine rows][64 fine columns] float2   (NBUF x NB x 1024 KL)
@@ -261,6 +267,7 @@ struct FuseWarp {
     float2 ge, go;
     float4 ze[NC], zo[NC];
   };
+  Pair nxt;  // FLLF_FUSE_PIPE: the next pair, read from the ring one step ahead
   __device__ __forceinline__ void read(Pair& d) {
     const uint32_t sl = ring + sr;
     sr = sr + SLOT == DEPTH * SLOT ? 0 : sr + SLOT;
@@ -442,9 +449,15 @@ struct FuseWarp {
                                        const float4 (&Dm2e)[NC], const float4 (&Dm2o)[NC], const float4& Dm2g) {
     if (t + PD < np) issue();
     cp_async_commit();
-    cp_async_wait<PD>();
     Pair d;
-    read(d);
+    if (FLLF_FUSE_PIPE) {  // pair t was read one step ahead; read pair t+1 now
+      d = nxt;
+      cp_async_wait<PD - 1>();
+      if (t + 1 < np) read(nxt);
+    } else {
+      cp_async_wait<PD>();
+      read(d);
+    }
     if (EMIT) emit<OWN>(d, Wn);
     if (VSTEP) vstep(d);
     if (VC) {
@@ -477,6 +490,10 @@ struct FuseWarp {
     for (int i = 0; i < PD; ++i) {
       if (i < np) issue();
       cp_async_commit();
+    }
+    if (FLLF_FUSE_PIPE) {
+      cp_async_wait<PD - 1>();
+      read(nxt);
     }
     float2 CA[NC], CB[NC], CC[NC];
     float4 ZAe[NC], ZAo[NC], ZBe[NC], ZBo[NC], ZCe[NC], ZCo[NC];

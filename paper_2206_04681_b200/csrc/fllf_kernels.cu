@@ -414,6 +414,9 @@ __global__ void __launch_bounds__(32) k_build(const BuildParams P) {
 //  * up to 8 orders per warp (amortises the per-pixel sincos + chunk-start
 //    phasor); I rows prefetched PD pairs ahead;
 //  * 32-bit in-frame offsets; halo-column stores only in edge warps.
+#ifndef FLLF_B0_PIPE
+#define FLLF_B0_PIPE 1
+#endif
 template <int NC, bool EDGE>
 struct Build0Warp {
   const BuildParams& P;
@@ -609,6 +612,22 @@ struct Build0Warp {
     cp_async_wait<PD - 1>();
     proc<false, false>(read_pair(1), 0);
     if (PD + 1 <= R + 1) issue_pair(PD + 1); else cp_async_commit();
+#if FLLF_B0_PIPE
+    // pair p+1 is read from the ring before pair p is processed (the wait is
+    // a compiler fence: this keeps the shared-memory load latency off the
+    // start of every pair)
+    cp_async_wait<PD - 1>();
+    Pair d = read_pair(2);
+#pragma unroll 1
+    for (int p = 2; p <= R; ++p) {
+      if (p + PD <= R + 1) issue_pair(p + PD); else cp_async_commit();
+      cp_async_wait<PD - 1>();
+      const Pair nd = read_pair(p + 1);
+      proc<true, false>(d, o0 + p - 2);
+      d = nd;
+    }
+    proc<true, true>(d, o0 + R - 1);
+#else
 #pragma unroll 1
     for (int p = 2; p <= R; ++p) {
       cp_async_wait<PD - 1>();
@@ -618,6 +637,7 @@ struct Build0Warp {
     }
     cp_async_wait<PD - 1>();
     proc<true, true>(read_pair(R + 1), o0 + R - 1);
+#endif
     cp_async_wait<0>();
   }
 };
@@ -1107,6 +1127,11 @@ constexpr int kApply0Unroll = FLLF_A0_UNROLL;
 #define FLLF_A1_UNROLL 1
 #endif
 constexpr int kApply1Unroll = FLLF_A1_UNROLL;  // levels >= 1 (A/B knob)
+// K-specialised level-0 order loop software-pipelined across ring stages (A/B knob)
+#ifndef FLLF_APPLY_PIPE
+#define FLLF_APPLY_PIPE 1
+#endif
+constexpr bool kApplyPipe = FLLF_APPLY_PIPE != 0;
 // KT > 0 (level 0): a whole tile's orders in a ring of K/2 stages when that
 // is 6..8 (the ring then restarts at the same stage every tile)
 template <bool LEVEL0, bool MAPS = false, int KT = 0>
@@ -1399,18 +1424,29 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0, MAPS>()) k_apply_cl
 
     // one order from stage slot `so` (order-local base): bn holds b_{k+2} on
     // entry and b_k on exit, bp = b_{k+1}
-    auto order = [&](int i, const unsigned char* so, float2 (&bn)[8], const float2 (&bp)[8]) {
-      const float4 x0 = *reinterpret_cast<const float4*>(so);
-      const float4 x1 = *reinterpret_cast<const float4*>(so + CROW_BYTES);
-      const float4 x2 = *reinterpret_cast<const float4*>(so + 2 * CROW_BYTES);
-      float4 fz[4];
+    // one order's stage data in registers: coarse rows r-1, r, r+1 (and the
+    // fine Z rows for levels >= 1)
+    struct OrderIn {
+      float4 x0, x1, x2;
+      float4 fz[LEVEL0 ? 1 : 4];
+    };
+    auto load_order = [&](const unsigned char* so) {
+      OrderIn d;
+      d.x0 = *reinterpret_cast<const float4*>(so);
+      d.x1 = *reinterpret_cast<const float4*>(so + CROW_BYTES);
+      d.x2 = *reinterpret_cast<const float4*>(so + 2 * CROW_BYTES);
       if (!LEVEL0) {
         const unsigned char* sf = so + (rowf - rowc);
-        fz[0] = *reinterpret_cast<const float4*>(sf);
-        fz[1] = *reinterpret_cast<const float4*>(sf + 16);
-        fz[2] = *reinterpret_cast<const float4*>(sf + FROW_BYTES);
-        fz[3] = *reinterpret_cast<const float4*>(sf + FROW_BYTES + 16);
+        d.fz[0] = *reinterpret_cast<const float4*>(sf);
+        d.fz[1] = *reinterpret_cast<const float4*>(sf + 16);
+        d.fz[2] = *reinterpret_cast<const float4*>(sf + FROW_BYTES);
+        d.fz[3] = *reinterpret_cast<const float4*>(sf + FROW_BYTES + 16);
       }
+      return d;
+    };
+    auto order_in = [&](int i, const OrderIn& d, float2 (&bn)[8], const float2 (&bp)[8]) {
+      const float4 x0 = d.x0, x1 = d.x1, x2 = d.x2;
+      const float4* fz = d.fz;
       // vertical: even fine row (x_{r-1} + 6 x_r + x_{r+1}), odd (x_r + x_{r+1}); columns a = 2j, b = 2j+1
       const float2 vea = pfma(bc(6.f), lo2(x1), padd(lo2(x0), lo2(x2)));
       const float2 veb = pfma(bc(6.f), hi2(x1), padd(hi2(x0), hi2(x2)));
@@ -1463,6 +1499,9 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0, MAPS>()) k_apply_cl
         }
       }
     };
+    auto order = [&](int i, const unsigned char* so, float2 (&bn)[8], const float2 (&bp)[8]) {
+      order_in(i, load_order(so), bn, bp);
+    };
     auto stage_wait = [&]() -> const unsigned char* {
       mbar_wait_parity(&full[s], ph);
       return rowc + s * STAGE;
@@ -1478,7 +1517,34 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0, MAPS>()) k_apply_cl
 
     int i = KL - 1;
     constexpr bool kFull = KT > 0 && OPS == 2 && (KT % 2) == 0 && (S % (KT / 2)) == 0;
-    if constexpr (kFull) {
+    if constexpr (kFull && kApplyPipe && !MAPS) {  // (MAPS: spills at 128 registers)
+      // software-pipelined: the next stage's wait and shared-memory loads are
+      // issued before the current stage's second order is evaluated (the
+      // barrier wait is a compiler fence, so without this every stage starts
+      // with an exposed LDS + shuffle latency)
+      const unsigned char* rs = rowc + s * STAGE;
+      const uint32_t fb = smem_u32(&full[s]), eb = smem_u32(&empty[s]);
+      mbar_wait_u32(fb, ph);
+      OrderIn oa = load_order(rs), ob = load_order(rs + OBYTES);
+#pragma unroll
+      for (int jst = 0; jst < KT / 2; ++jst) {
+        order_in(KT - 1 - 2 * jst, oa, b2, b1);
+        if (jst + 1 < KT / 2) {
+          mbar_wait_u32(fb + (jst + 1) * 8, ph);
+          oa = load_order(rs + (jst + 1) * STAGE);
+        }
+        order_in(KT - 2 - 2 * jst, ob, b1, b2);
+        __syncwarp();
+        if (lane == 0) mbar_arrive_u32(eb + jst * 8);
+        if (jst + 1 < KT / 2) ob = load_order(rs + (jst + 1) * STAGE + OBYTES);
+      }
+      s += KT / 2;
+      if (s == S) {
+        s = 0;
+        ph ^= 1u;
+      }
+      i = -1;
+    } else if constexpr (kFull) {
       const unsigned char* rs = rowc + s * STAGE;
       const uint32_t fb = smem_u32(&full[s]), eb = smem_u32(&empty[s]);
 #pragma unroll
