@@ -118,8 +118,9 @@ __device__ __forceinline__ void sts2(uint32_t a, float2 v) {
 #endif
 constexpr int FUSE_NBUF = FLLF_FUSE_NBUF;
 // read each ring pair into registers one step ahead (the cp.async wait is a
-// compiler fence).  Off: with the Z_l delay line of 3 pairs already in
-// registers the extra pair spills (92-184 bytes at 128 registers).
+// compiler fence); K = 16 only, where it fits 128 registers once the
+// coefficient pairs come from the kernel parameters.  Off: measured 10 %
+// slower at config 5 level 1 (1.51-1.53 vs 1.38-1.39 ms); A/B knob.
 #ifndef FLLF_FUSE_PIPE
 #define FLLF_FUSE_PIPE 0
 #endif
@@ -169,7 +170,14 @@ struct FuseWarp {
   uint32_t crow;        // C[0][il0][0][2 lane] (shared address)
   uint32_t gbrow;       // Gb[0][0][2 lane]
   int jn;               // fine row pair of the next issue (reflected path)
-  float2 cwk[NC][4];    // this warp's Clenshaw coefficient pairs (ApplyParams::cw)
+  // PIPE: each ring pair is read one step ahead (K = 16, one order per warp:
+  // the other instantiations spill).  This warp's Clenshaw coefficient pairs
+  // (ApplyParams::cw) are then read from the kernel parameters at each use
+  // instead of being held in registers.
+  static constexpr bool PIPE = FLLF_FUSE_PIPE && KT == 16 && NC == 1;
+  int il0_;
+  float2 cwk_[PIPE ? 1 : NC][4];
+  __device__ __forceinline__ float2 cwk(int i, int u) const { return PIPE ? P.cw[il0_ + i][u] : cwk_[i][u]; }
   int cb_;
   uint32_t sbase_;
   float* dbase;         // D_l of the frame
@@ -192,6 +200,7 @@ struct FuseWarp {
     halo_l = EDGE && store_lane && x == 1;
     halo_r = EDGE && store_lane && x == ((P.Wf & 1) ? P.Wc - 2 : P.Wc - 1);
     const int il0 = warp * NC;
+    il0_ = il0;
     zks = P.src.kstride_z;
     gpitch = P.src.pitch;
     zpitch = P.src.zpitch;
@@ -208,7 +217,8 @@ struct FuseWarp {
 #pragma unroll
     for (int i = 0; i < NC; ++i) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) cwk[i][u] = P.cw[il0 + i][u];
+      for (int u = 0; u < 4; ++u)
+        if (!PIPE) cwk_[i][u] = P.cw[il0 + i][u];
       Pc[i][0] = Pc[i][1] = Ac[i][0] = Ac[i][1] = make_float2(0.f, 0.f);
     }
     Pr = Ar = make_float2(0.f, 0.f);
@@ -342,10 +352,10 @@ struct FuseWarp {
       const float2 vo = padd(C0[i], Cp[i]);
       const float2 veL = shfl_up2(ve), veR = shfl_down2(ve), voL = shfl_up2(vo), voR = shfl_down2(vo);
       // horizontal + polyphase scales and a_k with the sign pattern (cwk)
-      const float2 c0 = pfma(pfma(bc(6.f), ve, padd(veL, veR)), cwk[i][0], pmul(lo2(ze[i]), cwk[i][3]));
-      const float2 c1 = pfma(padd(ve, veR), cwk[i][1], pmul(hi2(ze[i]), cwk[i][3]));
-      const float2 c2 = pfma(pfma(bc(6.f), vo, padd(voL, voR)), cwk[i][1], pmul(lo2(zo[i]), cwk[i][3]));
-      const float2 c3 = pfma(padd(vo, voR), cwk[i][2], pmul(hi2(zo[i]), cwk[i][3]));
+      const float2 c0 = pfma(pfma(bc(6.f), ve, padd(veL, veR)), cwk(i, 0), pmul(lo2(ze[i]), cwk(i, 3)));
+      const float2 c1 = pfma(padd(ve, veR), cwk(i, 1), pmul(hi2(ze[i]), cwk(i, 3)));
+      const float2 c2 = pfma(pfma(bc(6.f), vo, padd(voL, voR)), cwk(i, 1), pmul(lo2(zo[i]), cwk(i, 3)));
+      const float2 c3 = pfma(padd(vo, voR), cwk(i, 2), pmul(hi2(zo[i]), cwk(i, 3)));
       sts4(cb + i * 1024, cat4(c0, c1));
       sts4(cb + i * 1024 + 512, cat4(c2, c3));
     }
@@ -450,7 +460,7 @@ struct FuseWarp {
     if (t + PD < np) issue();
     cp_async_commit();
     Pair d;
-    if (FLLF_FUSE_PIPE) {  // pair t was read one step ahead; read pair t+1 now
+    if (PIPE) {  // pair t was read one step ahead; read pair t+1 now
       d = nxt;
       cp_async_wait<PD - 1>();
       if (t + 1 < np) read(nxt);
@@ -491,7 +501,7 @@ struct FuseWarp {
       if (i < np) issue();
       cp_async_commit();
     }
-    if (FLLF_FUSE_PIPE) {
+    if (PIPE) {
       cp_async_wait<PD - 1>();
       read(nxt);
     }

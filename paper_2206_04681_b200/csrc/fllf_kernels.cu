@@ -1132,6 +1132,10 @@ constexpr int kApply1Unroll = FLLF_A1_UNROLL;  // levels >= 1 (A/B knob)
 #define FLLF_APPLY_PIPE 1
 #endif
 constexpr bool kApplyPipe = FLLF_APPLY_PIPE != 0;
+#ifndef FLLF_APPLY_PIPE_MAPS
+#define FLLF_APPLY_PIPE_MAPS 0
+#endif
+constexpr bool kApplyPipeMaps = FLLF_APPLY_PIPE_MAPS != 0;
 // KT > 0 (level 0): a whole tile's orders in a ring of K/2 stages when that
 // is 6..8 (the ring then restarts at the same stage every tile)
 template <bool LEVEL0, bool MAPS = false, int KT = 0>
@@ -1517,7 +1521,7 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0, MAPS>()) k_apply_cl
 
     int i = KL - 1;
     constexpr bool kFull = KT > 0 && OPS == 2 && (KT % 2) == 0 && (S % (KT / 2)) == 0;
-    if constexpr (kFull && kApplyPipe && !MAPS) {  // (MAPS: spills at 128 registers)
+    if constexpr (kFull && kApplyPipe && (!MAPS || kApplyPipeMaps)) {  // (MAPS: 20-24 bytes of spills)
       // software-pipelined: the next stage's wait and shared-memory loads are
       // issued before the current stage's second order is evaluated (the
       // barrier wait is a compiler fence, so without this every stage starts
