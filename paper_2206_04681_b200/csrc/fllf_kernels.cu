@@ -457,7 +457,10 @@ struct Build0Warp {
   };
   // I rows are staged through a per-warp shared-memory ring with cp.async:
   // PD row pairs in flight without holding them in registers.
-  static constexpr int PD = 8;
+#ifndef FLLF_B0_PD
+#define FLLF_B0_PD 8
+#endif
+  static constexpr int PD = FLLF_B0_PD;
   float2 (*ring)[2][32];
   // issue the copies of pair p (rows 2(o0+p-1), +1; p = 0: the two halo rows above)
   // rows_in: no row of this strip's reads (incl. the prefetch overrun) needs
