@@ -565,7 +565,7 @@ struct FuseWarp {
 template <int NC, int PD, bool EDGE, bool ROWS_IN, int KT>
 __device__ __forceinline__ void fuse_run(const FuseParams& P, int cb, int o0, int R, int frame, int nw, int warp,
                                          uint32_t sbase, uint32_t bars) {
-  if (warp == 0) {
+  if (warp == 0 && !(P.exp & 4)) {  // (exp bit 4, timing only: no warp builds G)
     FuseWarp<NC, PD, EDGE, true, ROWS_IN, KT> w(P, cb, o0, R, frame, nw, warp, sbase, bars);
     w.run();
   } else {
@@ -704,7 +704,7 @@ cudaError_t launch_fuse_nc(const FuseParams& p0, int batch, cudaStream_t s, bool
   int R = std::min(rmax, p.Hc);
   while (R > 4 && (long long)bx * ((p.Hc + R - 1) / R) * batch < target_ctas) R = (R + 1) / 2;
   p.rows_per_strip = R;
-  static const int exp = [] {  // A/B experiments: 1 = no order sums, 2 = no coefficients (timing only)
+  static const int exp = [] {  // A/B experiments (timing only): 1 = no order sums, 2 = no coefficients, 4 = no G warp
     const char* e = std::getenv("FLLF_FUSE_EXP");
     return e ? std::atoi(e) : 0;
   }();
