@@ -117,6 +117,13 @@ __device__ __forceinline__ void sts2(uint32_t a, float2 v) {
 #define FLLF_FUSE_NBUF 1
 #endif
 constexpr int FUSE_NBUF = FLLF_FUSE_NBUF;
+// G_l (the real channel: G_{l+1} and the g of the order sums) built by a
+// 17th warp instead of by warp 0 on top of its order: warp 0 no longer sets
+// the pace of the CTA's batch barriers (one order per warp only; A/B knob)
+#ifndef FLLF_FUSE_GWARP
+#define FLLF_FUSE_GWARP 1
+#endif
+constexpr bool FUSE_GWARP = FLLF_FUSE_GWARP != 0;
 // read each ring pair into registers one step ahead (the cp.async wait is a
 // compiler fence); K = 16 only, where it fits 128 registers once the
 // coefficient pairs come from the kernel parameters.  Off: measured 10 %
@@ -128,11 +135,14 @@ constexpr int FUSE_NBUF = FLLF_FUSE_NBUF;
 // Shared-memory layout of one CTA (bytes), NB = fuse_nb(warps):
 //   C    [NBUF][NB pairs][KL orders][2 fine rows][64 fine columns] float2   (NBUF x NB x 1024 KL)
 //   Gb   [NBUF][NB pairs][2 fine rows][64 fine columns] float                 (NBUF x NB x 512)
-//   ring of warp 0:  DEPTH slots x (G 512 + Z 1024 NC)
-//   ring of warp w:  DEPTH slots x Z 1024 NC
+//   GW = 0: ring of warp 0:  DEPTH slots x (G 512 + Z 1024 NC)
+//           ring of warp w:  DEPTH slots x Z 1024 NC
+//   GW = 1: ring of order warp w (0 .. KL/NC - 1): DEPTH slots x Z 1024 NC,
+//           then the G warp's (warp KL/NC): DEPTH slots x G 512
 template <int NC, int PD>
 struct FuseLayout {
   static constexpr int NBUF = NC == 1 ? FUSE_NBUF : 1;  // (two orders per warp: K > 16, shared memory)
+  static constexpr bool GW = FUSE_GWARP && NC == 1;      // G_l built by a warp of its own
   static constexpr int DEPTH = PD + 1;
   static constexpr int ZSLOT = NC * 1024;  // NC orders x 2 rows x 32 lanes x float4
   static constexpr int G0SLOT = 512 + ZSLOT;
@@ -140,18 +150,21 @@ struct FuseLayout {
   __host__ __device__ static int g_buf(int KL) { return fuse_nb(KL / NC) * 512; }
   __host__ __device__ static int g_off(int KL) { return NBUF * c_buf(KL); }
   __host__ __device__ static int ring_off(int KL, int w) {
+    if (GW) return g_off(KL) + NBUF * g_buf(KL) + w * DEPTH * ZSLOT;  // (w = KL/NC: the G warp)
     return g_off(KL) + NBUF * g_buf(KL) + (w == 0 ? 0 : DEPTH * G0SLOT + (w - 1) * DEPTH * ZSLOT);
   }
-  __host__ __device__ static int smem(int KL) { return ring_off(KL, KL / NC); }
+  __host__ __device__ static int smem(int KL) { return ring_off(KL, KL / NC) + (GW ? DEPTH * 512 : 0); }
+  __host__ __device__ static int warps(int KL) { return KL / NC + (GW ? 1 : 0); }
 };
 
 // ---- one warp: NC orders of the strip (DO_G: warp 0 also builds G;
 // ROWS_IN: no fine row of the strip needs reflection)
-template <int NC, int PD, bool EDGE, bool DO_G, bool ROWS_IN, int KT>
+template <int NC, int PD, bool EDGE, bool DO_G, bool ROWS_IN, int KT, bool HAS_Z = true>
 struct FuseWarp {
   using L = FuseLayout<NC, PD>;
   static constexpr int DEPTH = L::DEPTH;
-  static constexpr int SLOT = DO_G ? L::G0SLOT : L::ZSLOT;
+  static constexpr int SLOT = (DO_G ? 512 : 0) + (HAS_Z ? L::ZSLOT : 0);
+  static constexpr int NZ = HAS_Z ? NC : 0;  // complex orders of this warp (0: the G warp)
   static constexpr int ZOFF = DO_G ? 512 : 0;
   // the plan's order count (compile time for KT > 0)
   __device__ __forceinline__ int kl() const { return KT > 0 ? KT : P.KL; }
@@ -174,10 +187,13 @@ struct FuseWarp {
   // the other instantiations spill).  This warp's Clenshaw coefficient pairs
   // (ApplyParams::cw) are then read from the kernel parameters at each use
   // instead of being held in registers.
+  // (With the G warp of its own, GW, the order warps have the registers to
+  // keep the pairs.)
   static constexpr bool PIPE = FLLF_FUSE_PIPE && KT == 16 && NC == 1;
+  static constexpr bool CW_PARAM = PIPE && !L::GW;
   int il0_;
-  float2 cwk_[PIPE ? 1 : NC][4];
-  __device__ __forceinline__ float2 cwk(int i, int u) const { return PIPE ? P.cw[il0_ + i][u] : cwk_[i][u]; }
+  float2 cwk_[CW_PARAM ? 1 : NC][4];
+  __device__ __forceinline__ float2 cwk(int i, int u) const { return CW_PARAM ? P.cw[il0_ + i][u] : cwk_[i][u]; }
   int cb_;
   uint32_t sbase_;
   float* dbase;         // D_l of the frame
@@ -215,10 +231,10 @@ struct FuseWarp {
     gbrow = smem + L::g_off(kl()) + lane * 8;
     jn = o0 - 2;
 #pragma unroll
-    for (int i = 0; i < NC; ++i) {
+    for (int i = 0; i < NZ; ++i) {
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        if (!PIPE) cwk_[i][u] = P.cw[il0 + i][u];
+        if (!CW_PARAM && HAS_Z) cwk_[i][u] = P.cw[il0 + i][u];
       Pc[i][0] = Pc[i][1] = Ac[i][0] = Ac[i][1] = make_float2(0.f, 0.f);
     }
     Pr = Ar = make_float2(0.f, 0.f);
@@ -254,7 +270,7 @@ struct FuseWarp {
         }
       }
 #pragma unroll
-      for (int i = 0; i < NC; ++i) {
+      for (int i = 0; i < NZ; ++i) {
         const uint32_t zd = sl + ZOFF + (i * 2 + r) * 512 + lane * 16;
         const float2* q = zp + i * zks;
         if (EDGE) {
@@ -286,7 +302,7 @@ struct FuseWarp {
       d.go = lds2(sl + 256 + lane * 8);
     }
 #pragma unroll
-    for (int i = 0; i < NC; ++i) {
+    for (int i = 0; i < NZ; ++i) {
       d.ze[i] = lds4(sl + ZOFF + (i * 2) * 512 + lane * 16);
       d.zo[i] = lds4(sl + ZOFF + (i * 2 + 1) * 512 + lane * 16);
     }
@@ -297,7 +313,7 @@ struct FuseWarp {
   template <bool OWN>
   __device__ __forceinline__ void emit(const Pair& d, float2 (&h)[NC]) {
 #pragma unroll
-    for (int i = 0; i < NC; ++i) {
+    for (int i = 0; i < NZ; ++i) {
       const float2 ea = pfma(bc(W2), lo2(d.ze[i]), Pc[i][0]);
       const float2 eb = pfma(bc(W2), hi2(d.ze[i]), Pc[i][1]);
       h[i] = hfilt_c(ea, eb);
@@ -330,7 +346,7 @@ struct FuseWarp {
   }
   __device__ __forceinline__ void vstep(const Pair& d) {
 #pragma unroll
-    for (int i = 0; i < NC; ++i) {
+    for (int i = 0; i < NZ; ++i) {
       vstep_fixed(Pc[i][0], Ac[i][0], lo2(d.ze[i]), lo2(d.zo[i]));
       vstep_fixed(Pc[i][1], Ac[i][1], hi2(d.ze[i]), hi2(d.zo[i]));
     }
@@ -346,7 +362,7 @@ struct FuseWarp {
                                        int& q) {
     const uint32_t cb = crow + cbo + q * (kl() * 1024);
 #pragma unroll
-    for (int i = 0; i < NC; ++i) {
+    for (int i = 0; i < NZ; ++i) {
       // vertical up-sampling (unscaled): even fine row x_{i-1} + 6 x_i + x_{i+1}, odd x_i + x_{i+1}
       const float2 ve = pfma(bc(6.f), C0[i], padd(Cm[i], Cp[i]));
       const float2 vo = padd(C0[i], Cp[i]);
@@ -384,15 +400,15 @@ struct FuseWarp {
     const int n0 = FUSE_NB * bt;
     const int ub = L::NBUF == 2 ? (bt & 1) : 0;
     if (L::NBUF == 2) mbar_wait_u32(bars + 8 * ub, (bt >> 1) & 1);
-    else bar_sync_id(FUSE_BAR, nw * 32);
+    else bar_sync_id(FUSE_BAR, blockDim.x);
     if (!(P.exp & 1)) {
       const int KL = kl();
       const uint32_t cbase = sbase_ + ub * L::c_buf(KL);
       const int goff = L::g_off(KL) + ub * L::g_buf(KL);
       const int row0 = 2 * (o0 + n0);
-      const int slot = L::NBUF == 2 ? (warp + 4 * bt) % nw : warp;
+      const int slot = L::NBUF == 2 ? (warp + 4 * bt) % (blockDim.x / 32) : warp;
 #pragma unroll 1
-      for (int p = slot * 32 + lane; p < cnt * 128; p += nw * 32) {
+      for (int p = slot * 32 + lane; p < cnt * 128; p += blockDim.x) {
         const int q = p >> 7, r = (p >> 6) & 1, f = p & 63;
         const float g = lds1(sbase_ + goff + ((q * 2 + r) * 64 + f) * 4);
         float sn, c1;
@@ -435,7 +451,7 @@ struct FuseWarp {
       }
     }
     if (L::NBUF == 2) mbar_arrive_u32(bars + 16 + 8 * ub);
-    else bar_sync_id(FUSE_BAR, nw * 32);
+    else bar_sync_id(FUSE_BAR, blockDim.x);
   }
 
   // NBUF = 2: before the first coefficients of batch bt, wait until the order
@@ -478,7 +494,7 @@ struct FuseWarp {
       }
     }
 #pragma unroll
-    for (int i = 0; i < NC; ++i) {
+    for (int i = 0; i < NZ; ++i) {
       De[i] = d.ze[i];
       Do[i] = d.zo[i];
     }
@@ -509,7 +525,7 @@ struct FuseWarp {
     float4 ZAe[NC], ZAo[NC], ZBe[NC], ZBo[NC], ZCe[NC], ZCo[NC];
     float4 GA = make_float4(0.f, 0.f, 0.f, 0.f), GB = GA, GC = GA;
 #pragma unroll
-    for (int i = 0; i < NC; ++i) {
+    for (int i = 0; i < NZ; ++i) {
       CA[i] = CB[i] = CC[i] = make_float2(0.f, 0.f);
       ZAe[i] = ZAo[i] = ZBe[i] = ZBo[i] = ZCe[i] = ZCo[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
@@ -565,7 +581,15 @@ struct FuseWarp {
 template <int NC, int PD, bool EDGE, bool ROWS_IN, int KT>
 __device__ __forceinline__ void fuse_run(const FuseParams& P, int cb, int o0, int R, int frame, int nw, int warp,
                                          uint32_t sbase, uint32_t bars) {
-  if (warp == 0 && !(P.exp & 4)) {  // (exp bit 4, timing only: no warp builds G)
+  if (FuseLayout<NC, PD>::GW) {
+    if (warp == nw) {  // the G warp
+      FuseWarp<NC, PD, EDGE, true, ROWS_IN, KT, false> w(P, cb, o0, R, frame, nw, warp, sbase, bars);
+      w.run();
+    } else {
+      FuseWarp<NC, PD, EDGE, false, ROWS_IN, KT> w(P, cb, o0, R, frame, nw, warp, sbase, bars);
+      w.run();
+    }
+  } else if (warp == 0 && !(P.exp & 4)) {  // (exp bit 4, timing only: no warp builds G)
     FuseWarp<NC, PD, EDGE, true, ROWS_IN, KT> w(P, cb, o0, R, frame, nw, warp, sbase, bars);
     w.run();
   } else {
@@ -577,7 +601,8 @@ __device__ __forceinline__ void fuse_run(const FuseParams& P, int cb, int o0, in
 // KT > 0: the plan's order count at compile time (16 or 8; the order sums'
 // Clenshaw loop unrolls completely, the layout offsets fold)
 template <int NC, int PD, int KT = 0>
-__global__ void __launch_bounds__(FUSE_MAX_WARPS * 32, 1) k_fuse(const __grid_constant__ FuseParams P) {
+__global__ void __launch_bounds__((FUSE_MAX_WARPS + (FuseLayout<NC, PD>::GW ? 1 : 0)) * 32, 1)
+    k_fuse(const __grid_constant__ FuseParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar[4];  // NBUF = 2: full[2], empty[2] of the order-sum buffers
   if (FuseLayout<NC, PD>::NBUF == 2) {
@@ -711,7 +736,7 @@ cudaError_t launch_fuse_nc(const FuseParams& p0, int batch, cudaStream_t s, bool
   p.exp = exp;
   const int smem = FuseLayout<NC, PD>::smem(p.KL);
   dim3 grid(bx, (p.Hc + R - 1) / R, batch);
-  const dim3 block(32 * (p.KL / NC));
+  const dim3 block(32 * FuseLayout<NC, PD>::warps(p.KL));
   static DeviceFlags attr0, attr8, attr16;
   cudaError_t e;
   if (NC == 1 && p.KL == 16) {
