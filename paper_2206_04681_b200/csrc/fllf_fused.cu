@@ -21,12 +21,15 @@
 // compute the same D planes (exact algebra, different rounding order only).
 //
 // k_fuse layout.  CTA = one strip (R coarse rows x 28 coarse columns of one
-// frame) with one warp per NC orders (NC = 1 for K <= 16: 16 warps).  Warp w
+// frame) with one warp per NC orders (NC = 1 for K <= 16: 16 warps, plus a
+// 17th warp that builds only the real channel G_l -> G_{l+1} and stages the
+// g values of the order sums, FUSE_GWARP; with NC = 2 warp 0 does that on
+// top of its orders).  Warp w
 // owns the NC orders [w NC, (w+1) NC) of the plan's order range; lane L holds
 // coarse column x = 28 cb + L - 2 and fine columns 2x, 2x+1 (reflect-101 per
 // lane at the frame borders).  It streams fine row pairs P_j = (2j, 2j+1),
 // j = o0-2 .. o0+R+1, through its own shared-memory ring (cp.async, PD pairs
-// ahead; warp 0 also stages G_l): the VERTICAL 5-tap with two rolling
+// ahead; the G warp stages G_l): the VERTICAL 5-tap with two rolling
 // accumulators per order and column, then the HORIZONTAL 5-tap on the
 // finished coarse row from warp shuffles (k_build's arithmetic, so G_{l+1}
 // and Z_{l+1} are bit-identical to design AB).  Lanes 1..30 hold valid coarse
