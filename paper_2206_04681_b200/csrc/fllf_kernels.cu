@@ -417,12 +417,22 @@ __global__ void __launch_bounds__(32) k_build(const BuildParams P) {
 #ifndef FLLF_B0_PIPE
 #define FLLF_B0_PIPE 1
 #endif
+// two-chunk order interleaving (odd / even orders, no chunk-start sincos):
+// measured 1-3 % slower at config 5 (1.24-1.27 vs 1.22-1.23 ms), off; A/B knob
+#ifndef FLLF_B0_INTERLEAVE
+#define FLLF_B0_INTERLEAVE 0
+#endif
 template <int NC, bool EDGE>
 struct Build0Warp {
   const BuildParams& P;
   int o0, x, c0, rc0, rc1;
   bool store_lane, halo_l, halo_r, do_real, zfirst;
   int g0;
+  // inter: two chunks over orders 1 .. 2 NC interleaved -- chunk 0 the odd
+  // orders, chunk 1 the even ones, each a step-2 recurrence in 2 theta whose
+  // start phasors come from the one sincos of theta (no chunk-start sincos)
+  bool inter, odd;
+  int kst;  // planes between consecutive orders of this chunk
   const float* isrc;
   long long ipitch;
   float* gdst;
@@ -438,6 +448,9 @@ struct Build0Warp {
     c0 = 2 * x;
     rc0 = EDGE ? refl101(c0, P.Wf) : c0;
     rc1 = EDGE ? refl101(c0 + 1, P.Wf) : c0 + 1;
+    inter = FLLF_B0_INTERLEAVE && P.kbase == 1 && P.nchunks == 2;
+    odd = chunk == 0;
+    kst = inter ? 2 : 1;
     g0 = P.kbase + chunk * NC;
     zfirst = g0 == 1;  // chunks starting at order 1 need no chunk-start phasor
     do_real = chunk == 0;
@@ -446,7 +459,7 @@ struct Build0Warp {
     isrc = P.img.p + frame * P.img.fstride;
     ipitch = P.img.pitch;
     gdst = P.dst.G + frame * P.dst.fstride_r;
-    zdst = P.dst.Z + frame * P.dst.fstride_z + (long long)(chunk * NC) * P.dst.kstride_z;
+    zdst = P.dst.Z + frame * P.dst.fstride_z + (long long)(inter ? chunk : chunk * NC) * P.dst.kstride_z;
 #pragma unroll
     for (int i = 0; i < NC; ++i) Pc[i][0] = Pc[i][1] = Ac[i][0] = Ac[i][1] = make_float2(0.f, 0.f);
     Pr = Ar = make_float2(0.f, 0.f);
@@ -545,7 +558,17 @@ struct Build0Warp {
       float sn, cs;
       sincos_turns(I4[u], P.invT, &sn, &cs);
       tc[u] = 2.f * cs;
-      if (zfirst) {
+      if (inter) {  // step 2 theta: z_{k+2} = 2 cos(2 theta) z_k - z_{k-2}
+        const float c2 = fmaf(cs, cs, -sn * sn), s2 = 2.f * sn * cs;
+        tc[u] = 2.f * c2;
+        if (odd) {  // z_1, z_{-1}
+          zc[u] = make_float2(sn * (1.f / 256.f), cs * (1.f / 256.f));
+          zp[u] = make_float2(-sn * (1.f / 256.f), cs * (1.f / 256.f));
+        } else {  // z_2, z_0
+          zc[u] = make_float2(s2 * (1.f / 256.f), c2 * (1.f / 256.f));
+          zp[u] = make_float2(0.f, 1.f / 256.f);
+        }
+      } else if (zfirst) {
         zp[u] = make_float2(0.f, 1.f / 256.f);
         zc[u] = make_float2(sn * (1.f / 256.f), cs * (1.f / 256.f));
       } else {
@@ -564,7 +587,7 @@ struct Build0Warp {
         const float2 ea = padd(Pc[i][0], zc[0]);
         const float2 eb = padd(Pc[i][1], zc[1]);
         const float2 h = hsum_c(ea, eb);
-        float2* q = wide_off(zdst, (unsigned)(off0 + i * (int)P.dst.kstride_z));
+        float2* q = wide_off(zdst, (unsigned)(off0 + i * kst * (int)P.dst.kstride_z));
         if (store_lane) {
           FLLF_DBG_STORE(P, q, 8);
           stg2(q, h);
