@@ -54,3 +54,48 @@ def test_band_plan_errors(F):
         d = torch.zeros((128, 64), device="cuda")
         with pytest.raises(F.FllfError):
             p.apply(d, mode=F.FLLF_MAPS, sigma_map=d, m_map=d)
+
+
+@pytest.mark.parametrize("H,W,levels,K,P", [(2160, 3840, 7, 10, 2), (1080, 480, 6, 8, 4)])
+def test_bands_own_buffers(F, H, W, levels, K, P):
+    """Each band holds only its rows (+ the 2 halo rows above / below) in a
+    buffer of its own, as a rank of the multi-GPU band_filter does: the plan's
+    row-0 image pointer then lies below the allocation, and every TMA tensor
+    map must still cover only the rows the band reads / stores (DESIGN.md
+    section 11: such maps faulted before they were restricted)."""
+    from paper_2206_04681_b200 import dist as D
+    img = torch.from_numpy(synth.config2_image(seed=H + W + P, H=H, W=W)).cuda()
+    full = torch.empty_like(img)
+    with F.Plan(H, W, levels, K, 510.0, 30.0, 3.0) as p:
+        p.filter(img, full)
+    bands = [D.GpuBand(H, W, levels, K, 510.0, 30.0, 3.0, b) for b in D.band_partition(H, levels, P)]
+    try:
+        ins, outs = [], []
+        for gb in bands:
+            rb, re_ = gb.band
+            lo, hi = max(0, rb - 2), min(H, re_ + 2)
+            ins.append((img[lo:hi].clone(), rb - lo))
+            outs.append(torch.full((re_ - rb, W), float("nan"), device="cuda"))
+        torch.cuda.synchronize()
+        pitch = W * 4
+        for step in D.band_schedule(levels):
+            if step[0] == "xchg":
+                l = step[1]
+                for kind in step[2]:
+                    views = [gb.view(l, kind) for gb in bands]
+                    for i in range(len(bands) - 1):
+                        (vu, fu), (vd, fd) = views[i], views[i + 1]
+                        _, bot_u, _, send_dn_u, _, _ = D.halo_slices(fu, vu.shape[1], bands[i].own(l))
+                        top_d, _, send_up_d, _, _, _ = D.halo_slices(fd, vd.shape[1], bands[i + 1].own(l))
+                        vu[:, bot_u] = vd[:, send_up_d]
+                        vd[:, top_d] = vu[:, send_dn_u]
+            else:
+                for gb, (ib, top), ob in zip(bands, ins, outs):
+                    gb.run_step(step, ib.data_ptr() + top * pitch, pitch, ob.data_ptr(), pitch)
+        torch.cuda.synchronize()
+    finally:
+        for b in bands:
+            b.close()
+    out = torch.cat(outs)
+    assert torch.isfinite(out).all()
+    assert float((out - full).abs().max()) <= 1e-5
