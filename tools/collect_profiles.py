@@ -65,7 +65,7 @@ def main():
     for w in ("config2", "config4"):
         if os.path.exists(src(f"bench_{w}.err")):
             kernels(src(f"bench_{w}.err"), dst(f"bench_{w}_kernels.txt"))
-    for n in ("reference.json", "launches.csv", "clocks.csv", "gpu_tests.log"):
+    for n in ("reference.json", "launches.csv", "clocks.csv", "gpu_tests.log", "c5_full_raw.csv", "c2_full_raw.csv"):
         if os.path.exists(src(n)):
             shutil.copy(src(n), dst(n))
     import json
