@@ -1592,6 +1592,23 @@ __global__ void __launch_bounds__(160, apply_cl_ctas<LEVEL0, MAPS>()) k_apply_cl
         ph ^= 1u;
       }
       i = -1;
+    } else if constexpr (KT > 0 && OPS == 1 && (KT % S) == 0 && (KT % 2) == 0) {
+      // levels >= 1 with the order count at compile time (MAPS, K = 12): a
+      // tile consumes KT / S whole turns of the ring, so every tile starts
+      // at stage 0 and the loop unrolls with compile-time stage offsets and
+      // barrier addresses (one parity flip per turn)
+      const uint32_t fb = smem_u32(&full[0]), eb = smem_u32(&empty[0]);
+#pragma unroll
+      for (int jj = 0; jj < KT; ++jj) {
+        const int st = jj % S;
+        mbar_wait_u32(fb + st * 8, ph ^ (uint32_t)((jj / S) & 1));
+        if (jj & 1) order(KT - 1 - jj, rowc + st * STAGE, b1, b2);
+        else order(KT - 1 - jj, rowc + st * STAGE, b2, b1);
+        __syncwarp();
+        if (lane == 0) mbar_arrive_u32(eb + st * 8);
+      }
+      if ((KT / S) & 1) ph ^= 1u;
+      i = -1;
     } else if (OPS == 2) {
       constexpr int UNR = MAPS ? 1 : kApply0Unroll;  // MAPS: unrolling measured slower
 #pragma unroll UNR
@@ -1875,7 +1892,7 @@ static cudaError_t launch_apply_cl_t(const ApplyParams& p, int batch, cudaStream
     if (!generic && p.KL == 16) return launch_apply_cl_k<L0, HD, MP, 16>(p, batch, s, pdl);
     if (!generic && p.KL == 8) return launch_apply_cl_k<L0, HD, MP, 8>(p, batch, s, pdl);
   }
-  if constexpr (L0 && MP) {  // BASELINE configs[3]: K = 12
+  if constexpr (MP) {  // BASELINE configs[3]: K = 12 (level 0 and levels >= 1)
     if (!generic && p.KL == 12) return launch_apply_cl_k<L0, HD, MP, 12>(p, batch, s, pdl);
   }
   return launch_apply_cl_k<L0, HD, MP>(p, batch, s, pdl);
