@@ -163,12 +163,28 @@ def host_cores() -> int:
 
 
 def _oracle_job(job):
-    """One oracle run in a worker process (single-threaded numpy fp64):
-    (image, levels, K, T, sigma_r, m) -> seconds."""
-    img, levels, K, T, sig, m = job
+    """One oracle run in a worker process (single-threaded numpy fp64) -> seconds.
+    job = (image, levels, K, T, sigma_r, m) for the scalar workloads, or
+    (kind, payload, levels, K, T, params) with kind "maps" (Sec. III-B:
+    payload = (image, sigma_map, m_map)), "rgb" (payload = 3 channels, each
+    filtered) or "color" (payload = RGB, oracle/color_gain.enhance_rgb)."""
     from oracle import fllf_oracle as O
     t0 = time.perf_counter()
-    O.fourier_llf(img.astype(np.float64), levels, K, T, sig, m)
+    if isinstance(job[0], str):
+        kind, pay, levels, K, T, prm = job
+        if kind == "maps":
+            img, sig, mm = pay
+            O.fourier_llf(img.astype(np.float64), levels, K, T, sigma_map=sig.astype(np.float64),
+                          m_map=mm.astype(np.float64))
+        elif kind == "rgb":
+            for ch in pay:
+                O.fourier_llf(ch.astype(np.float64), levels, K, T, prm["sigma_r"], prm["m"])
+        else:
+            from oracle import color_gain as CG
+            CG.enhance_rgb(pay.astype(np.float64), levels, K, T, prm["sigma_r"], 5, 0.5, 3.0, 150.0)
+    else:
+        img, levels, K, T, sig, m = job
+        O.fourier_llf(img.astype(np.float64), levels, K, T, sig, m)
     return time.perf_counter() - t0
 
 
@@ -214,10 +230,27 @@ def run_reference(args):
     from paper_2206_04681_b200 import synth
     wl = WORKLOADS[args.workload]
     c = synth.CONFIGS[wl["cfg"]]
-    base = synth.config2_image(seed=2000 if wl["cfg"] == 2 else 5000)
     cores = host_cores()
-    crops = [base[(i // 4 % 4) * 270:(i // 4 % 4 + 1) * 270, (i % 4) * 480:(i % 4 + 1) * 480] for i in range(cores)]
-    jobs = [(cr, c["levels"], c["K"], c["T"], c["sigma_r"], c["m"]) for cr in crops]
+    win = [(slice((i // 4 % 4) * 270, (i // 4 % 4 + 1) * 270), slice((i % 4) * 480, (i % 4 + 1) * 480))
+           for i in range(cores)]
+    L, K, T = c["levels"], c["K"], c["T"]
+    if wl["cfg"] in (2, 5):
+        base = synth.config2_image(seed=2000 if wl["cfg"] == 2 else 5000)
+        jobs = [(base[w], L, K, T, c["sigma_r"], c["m"]) for w in win]
+    elif args.workload == "config4":
+        # maps drawn at crop size (same recipe and value ranges as the 4K maps)
+        base = synth.config2_image(seed=4000, H=c["H"], W=c["W"])
+        jobs = [("maps", (base[w], *synth.config4_maps(i % c["maps"], H=270, W=480)), L, K, T, None)
+                for i, w in enumerate(win)]
+    else:
+        rgb = synth.config3_rgb()
+        prm = {"sigma_r": c["sigma_r"], "m": c["m"]}
+        if args.workload == "config3":
+            jobs = [("rgb", [rgb[ch][w] for ch in range(3)], L, K, T, prm) for w in win]
+        elif args.workload == "color":
+            jobs = [("color", rgb[(slice(None), *w)], L, K, T, prm) for w in win]
+        else:  # bands: one gray 4K frame with the config-3 channel parameters
+            jobs = [(rgb[0][w], L, K, T, c["sigma_r"], c["m"]) for w in win]
     with _pool(cores) as pool:
         for _ in range(args.warmup):
             pool.map(_oracle_job, jobs)
@@ -227,8 +260,10 @@ def run_reference(args):
         dt = time.perf_counter() - t0
     px = args.steps * cores * 270 * 480
     v = px / 1e6 / dt
-    sample = (f"per step {cores} 270x480 crops (1/16 of a 1080x1920 frame each) of the {args.workload} "
-              f"workload, one per worker process on {cores} host cores")
+    extra = {"config4": ", each with its own (sigma_r, m) map pair drawn at crop size",
+             "config3": ", all 3 channels of each crop", "color": ", the whole YUV / gain-map pipeline"}
+    sample = (f"per step {cores} 270x480 crops of the {args.workload} workload's {c['H']}x{c['W']} input"
+              f"{extra.get(args.workload, '')}, one per worker process on {cores} host cores")
     line = {"metric": METRIC, "value": round(v, 4), "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * dt / args.steps, 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
