@@ -131,6 +131,16 @@ constexpr bool FUSE_GWARP = FLLF_FUSE_GWARP != 0;
 // compiler fence); K = 16 only, where it fits 128 registers once the
 // coefficient pairs come from the kernel parameters.  Off: measured 10 %
 // slower at config 5 level 1 (1.51-1.53 vs 1.38-1.39 ms); A/B knob.
+// Order sums of an even compile-time order count (KT) from k = 1 as two
+// interleaved half-length Clenshaw chains in 2 theta (even / odd orders)
+// instead of one chain in theta: same instruction count, half the dependent
+// latency of the phase the whole CTA waits for between its batch barriers.
+// Measured at config 5 (4 interleaved A/B pairs): level 1 1.41-1.46 ms with
+// it vs 1.39-1.43 ms without, so off; kept for A/B.
+#ifndef FLLF_FUSE_SPLIT
+#define FLLF_FUSE_SPLIT 0
+#endif
+
 #ifndef FLLF_FUSE_PIPE
 #define FLLF_FUSE_PIPE 0
 #endif
@@ -419,6 +429,32 @@ struct FuseWarp {
         const float2 tc = bc(2.f * c1);
         float2 b1 = make_float2(0.f, 0.f), b2 = b1;
         uint32_t a = cbase + ((q * KL + KL - 1) * 2 + r) * 512 + f * 8;
+        float res;
+#if FLLF_FUSE_SPLIT
+        if (KT > 0 && (KT & 1) == 0 && P.kbase == 1) {
+          // two independent half-length chains in phi = 2 theta (half the
+          // dependent latency between the batch barriers):
+          //   even k = 2j, j = 1..KT/2:  b_1 cos phi - b_2 + b_1' sin phi
+          //   odd  k = 2j+1 = j phi + theta, j = 0..KT/2-1: Clenshaw with
+          //   F_j = cos(j phi + theta), F_{-1} = F_0 = cos theta (sin: -G_{-1} = G_0),
+          //   sum = (b_0 - b_1) cos theta + (b_0' + b_1') sin theta
+          const float c2 = fmaf(c1, c1, -sn * sn), s2 = 2.f * sn * c1;
+          const float2 tc2 = bc(2.f * c2);
+          float2 e1 = make_float2(0.f, 0.f), e2 = e1, q1 = e1, q2 = e1;
+#pragma unroll
+          for (int t = 0; t < KT / 2; ++t) {
+            const float2 ce = lds2(a - (2 * t) * 1024), co = lds2(a - (2 * t + 1) * 1024);
+            const float2 ne = pfma(tc2, e1, padd(ce, pneg(e2)));
+            const float2 no = pfma(tc2, q1, padd(co, pneg(q2)));
+            e2 = e1;
+            e1 = ne;
+            q2 = q1;
+            q1 = no;
+          }
+          res = fmaf(e1.x, c2, fmaf(e1.y, s2, -e2.x)) + fmaf(q1.x - q2.x, c1, (q1.y + q2.y) * sn);
+        } else
+#endif
+        {
         int k = KL;
 #pragma unroll(KT > 0 ? 8 : 1)
         for (; k >= 4; k -= 4, a -= 4096) {
@@ -435,7 +471,6 @@ struct FuseWarp {
           b1 = nb2;
         }
         // b1 = b_{k0}, b2 = b_{k0+1}
-        float res;
         if (P.kbase == 1) {
           res = fmaf(b1.x, c1, fmaf(b1.y, sn, -b2.x));
         } else {
@@ -443,6 +478,7 @@ struct FuseWarp {
           sincos_turns_n(g, P.invT, P.kbase, &sk, &ck);
           const float cm = fmaf(ck, c1, sk * sn), sm = fmaf(sk, c1, -ck * sn);  // e^{i (k0-1) theta}
           res = fmaf(b1.x, ck, fmaf(b1.y, sk, -fmaf(b2.x, cm, b2.y * sm)));
+        }
         }
         const int row = row0 + 2 * q + r;
         const int col = 2 * (FUSE_COLS * cb_ - 2) + f;  // lanes 2..29 own f in [4, 60)
