@@ -145,6 +145,15 @@ constexpr bool FUSE_GWARP = FLLF_FUSE_GWARP != 0;
 #define FLLF_FUSE_PIPE 0
 #endif
 
+// Stream-loop iterations (of FUSE_NB = 3 pairs) per order-sum batch with one
+// order per warp and one hand-over buffer: 2 = batches of 6 pairs (768
+// pixels, two passes of the CTA's threads) between half as many CTA barrier
+// pairs, C twice as large (96 KB at K = 16).  Measured at config 5: no gain
+// in the step (4.33-4.38 vs 4.31-4.35 ms), so 1.
+#ifndef FLLF_FUSE_NBI
+#define FLLF_FUSE_NBI 1
+#endif
+
 // Shared-memory layout of one CTA (bytes), NB = fuse_nb(warps):
 //   C    [NBUF][NB pairs][KL orders][2 fine rows][64 fine columns] float2   (NBUF x NB x 1024 KL)
 //   Gb   [NBUF][NB pairs][2 fine rows][64 fine columns] float                 (NBUF x NB x 512)
@@ -155,12 +164,14 @@ constexpr bool FUSE_GWARP = FLLF_FUSE_GWARP != 0;
 template <int NC, int PD>
 struct FuseLayout {
   static constexpr int NBUF = NC == 1 ? FUSE_NBUF : 1;  // (two orders per warp: K > 16, shared memory)
+  static constexpr int NBI = (NC == 1 && NBUF == 1) ? FLLF_FUSE_NBI : 1;
+  static constexpr int NB = FUSE_NB * NBI;  // fine row pairs per order-sum batch
   static constexpr bool GW = FUSE_GWARP && NC == 1;      // G_l built by a warp of its own
   static constexpr int DEPTH = PD + 1;
   static constexpr int ZSLOT = NC * 1024;  // NC orders x 2 rows x 32 lanes x float4
   static constexpr int G0SLOT = 512 + ZSLOT;
-  __host__ __device__ static int c_buf(int KL) { return fuse_nb(KL / NC) * KL * 1024; }
-  __host__ __device__ static int g_buf(int KL) { return fuse_nb(KL / NC) * 512; }
+  __host__ __device__ static int c_buf(int KL) { return NB * KL * 1024; }
+  __host__ __device__ static int g_buf(int KL) { return NB * 512; }
   __host__ __device__ static int g_off(int KL) { return NBUF * c_buf(KL); }
   __host__ __device__ static int ring_off(int KL, int w) {
     if (GW) return g_off(KL) + NBUF * g_buf(KL) + w * DEPTH * ZSLOT;  // (w = KL/NC: the G warp)
@@ -410,7 +421,7 @@ struct FuseWarp {
   // the idle quarter (384 pixels, 512 threads) moves around.  NBUF = 1: two
   // CTA barriers.
   __device__ __forceinline__ void order_sum(int bt, int cnt) {
-    const int n0 = FUSE_NB * bt;
+    const int n0 = L::NB * bt;
     const int ub = L::NBUF == 2 ? (bt & 1) : 0;
     if (L::NBUF == 2) mbar_wait_u32(bars + 8 * ub, (bt >> 1) & 1);
     else bar_sync_id(FUSE_BAR, blockDim.x);
@@ -576,27 +587,35 @@ struct FuseWarp {
     step<false, false, true, false>(1, np, FUSE_PH1);
     step<true, false, true, false>(2, np, FUSE_PH2);
     step<true, true, true, false>(3, np, FUSE_PH0);
-    int t = 4, bt = 0;
+    int t = 4, bt = 0, it = 0;
 #pragma unroll 1
-    for (; t + 2 <= R + 2; t += 3, ++bt) {  // one batch bt (own pairs t-4 .. t-2) per iteration
-      q = 0;
-      begin_batch(bt);
+    for (; t + 2 <= R + 2; t += 3) {  // own pairs t-4 .. t-2; NBI iterations per batch bt
+      if (it == 0) {
+        q = 0;
+        begin_batch(bt);
+      }
       step<true, true, true, true>(t, np, FUSE_PH1);
       step<true, true, true, true>(t + 1, np, FUSE_PH2);
       step<true, true, true, true>(t + 2, np, FUSE_PH0);
-      end_batch(bt);
-      // NBUF = 2: the order sums run one batch behind the coefficients
-      if (L::NBUF == 2) {
-        if (bt > 0) order_sum(bt - 1, FUSE_NB);
-      } else {
-        order_sum(bt, FUSE_NB);
+      if (++it == L::NBI) {
+        end_batch(bt);
+        // NBUF = 2: the order sums run one batch behind the coefficients
+        if (L::NBUF == 2) {
+          if (bt > 0) order_sum(bt - 1, L::NB);
+        } else {
+          order_sum(bt, L::NB);
+        }
+        ++bt;
+        it = 0;
       }
     }
     // 0..2 steady steps remain (phase 1 first), then the last step t = R+3:
-    // the last (partial) batch
+    // the last (partial) batch, after the it iterations already in it
     const int rem = R + 3 - t;
-    q = 0;
-    begin_batch(bt);
+    if (it == 0) {
+      q = 0;
+      begin_batch(bt);
+    }
     if (rem == 0) {
       step<true, false, false, true>(t, np, FUSE_PH1);
     } else if (rem == 1) {
@@ -608,8 +627,8 @@ struct FuseWarp {
       step<true, false, false, true>(t + 2, np, FUSE_PH0);
     }
     end_batch(bt);
-    if (L::NBUF == 2 && bt > 0) order_sum(bt - 1, FUSE_NB);
-    order_sum(bt, rem + 1);
+    if (L::NBUF == 2 && bt > 0) order_sum(bt - 1, L::NB);
+    order_sum(bt, FUSE_NB * it + rem + 1);
 #undef FUSE_PH0
 #undef FUSE_PH1
 #undef FUSE_PH2
